@@ -1,0 +1,416 @@
+// libnmodl_b200_rt.so -- the C-ABI runtime under every generated mechanism.
+//
+// Plain pointers and sizes only (declared in include/nmodl_b200.h).  Python
+// binds it with ctypes (paper_1905_02241_b200/runtime.py); no PyTorch types
+// cross this boundary.  It owns what the reference leaves to "the simulator"
+// (modlc/codegen.py:59 "independent iterations"): device
+// memory for the SoA instance store, streams, CUDA-graph capture of the
+// per-timestep launch loop, the device status block, finiteness scans,
+// deterministic checksums for cross-GPU validation, and the node_index
+// scatter layout (stable counting sort by node).
+#include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "nmodl_b200/status.h"
+
+#define NMODL_API extern "C" __attribute__((visibility("default")))
+
+static thread_local char g_err[512];
+
+static int fail(cudaError_t e, const char* what) {
+  snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+  return (int)e;
+}
+#define CK(call)                                   \
+  do {                                             \
+    cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return fail(e_, #call); \
+  } while (0)
+
+NMODL_API const char* nmodl_last_error(void) { return g_err; }
+NMODL_API int nmodl_abi_version(void) { return 1; }
+
+// ---------------------------------------------------------------------------
+// device / memory / streams
+
+NMODL_API int nmodl_device_count(int* out) {
+  CK(cudaGetDeviceCount(out));
+  return 0;
+}
+NMODL_API int nmodl_set_device(int dev) {
+  CK(cudaSetDevice(dev));
+  return 0;
+}
+NMODL_API int nmodl_device_info(int dev, int* sm_count, long long* l2_bytes, long long* mem_bytes,
+                                int* cc_major, int* cc_minor, char* name, int name_len) {
+  cudaDeviceProp p;
+  CK(cudaGetDeviceProperties(&p, dev));
+  *sm_count = p.multiProcessorCount;
+  *l2_bytes = p.l2CacheSize;
+  *mem_bytes = (long long)p.totalGlobalMem;
+  *cc_major = p.major;
+  *cc_minor = p.minor;
+  if (name && name_len > 0) {
+    strncpy(name, p.name, name_len - 1);
+    name[name_len - 1] = 0;
+  }
+  return 0;
+}
+NMODL_API int nmodl_malloc(void** out, size_t bytes) {
+  CK(cudaMalloc(out, bytes ? bytes : 256));
+  return 0;
+}
+NMODL_API int nmodl_free(void* p) {
+  CK(cudaFree(p));
+  return 0;
+}
+NMODL_API int nmodl_host_alloc(void** out, size_t bytes) {
+  CK(cudaHostAlloc(out, bytes ? bytes : 64, cudaHostAllocPortable));
+  return 0;
+}
+NMODL_API int nmodl_host_free(void* p) {
+  CK(cudaFreeHost(p));
+  return 0;
+}
+NMODL_API int nmodl_host_register(void* p, size_t bytes) {
+  CK(cudaHostRegister(p, bytes, cudaHostRegisterPortable));
+  return 0;
+}
+NMODL_API int nmodl_host_unregister(void* p) {
+  CK(cudaHostUnregister(p));
+  return 0;
+}
+NMODL_API int nmodl_memcpy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+  return 0;
+}
+NMODL_API int nmodl_memcpy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+  return 0;
+}
+NMODL_API int nmodl_memcpy_d2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+NMODL_API int nmodl_memset(void* dst, int value, size_t bytes, cudaStream_t s) {
+  CK(cudaMemsetAsync(dst, value, bytes, s));
+  return 0;
+}
+NMODL_API int nmodl_stream_create(cudaStream_t* out) {
+  CK(cudaStreamCreateWithFlags(out, cudaStreamNonBlocking));
+  return 0;
+}
+NMODL_API int nmodl_stream_destroy(cudaStream_t s) {
+  CK(cudaStreamDestroy(s));
+  return 0;
+}
+NMODL_API int nmodl_stream_sync(cudaStream_t s) {
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+NMODL_API int nmodl_device_sync(void) {
+  CK(cudaDeviceSynchronize());
+  return 0;
+}
+NMODL_API int nmodl_event_create(cudaEvent_t* out) {
+  CK(cudaEventCreate(out));
+  return 0;
+}
+NMODL_API int nmodl_event_destroy(cudaEvent_t e) {
+  CK(cudaEventDestroy(e));
+  return 0;
+}
+NMODL_API int nmodl_event_record(cudaEvent_t e, cudaStream_t s) {
+  CK(cudaEventRecord(e, s));
+  return 0;
+}
+NMODL_API int nmodl_event_sync(cudaEvent_t e) {
+  CK(cudaEventSynchronize(e));
+  return 0;
+}
+NMODL_API int nmodl_event_elapsed_ms(cudaEvent_t a, cudaEvent_t b, float* ms) {
+  CK(cudaEventElapsedTime(ms, a, b));
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// CUDA graphs: the per-timestep launch loop (one kernel per step, v exogenous
+// between steps) is captured once and replayed, removing host launch cost.
+
+NMODL_API int nmodl_capture_begin(cudaStream_t s) {
+  CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  return 0;
+}
+NMODL_API int nmodl_capture_end(cudaStream_t s, cudaGraphExec_t* out) {
+  cudaGraph_t g;
+  CK(cudaStreamEndCapture(s, &g));
+  cudaError_t e = cudaGraphInstantiate(out, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(e, "cudaGraphInstantiate");
+  return 0;
+}
+NMODL_API int nmodl_graph_launch(cudaGraphExec_t g, cudaStream_t s) {
+  CK(cudaGraphLaunch(g, s));
+  return 0;
+}
+NMODL_API int nmodl_graph_destroy(cudaGraphExec_t g) {
+  CK(cudaGraphExecDestroy(g));
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// status block
+
+NMODL_API int nmodl_status_reset(nmodl_status* st, cudaStream_t s) {
+  nmodl_status h;
+  h.err_key = NMODL_NO_ERROR;
+  h.payload_key = NMODL_NO_ERROR;
+  h.payload = 0.0;
+  h.lock = 0;
+  h.reserved = 0;
+  CK(cudaMemcpyAsync(st, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+NMODL_API int nmodl_status_size(void) { return (int)sizeof(nmodl_status); }
+
+// ---------------------------------------------------------------------------
+// finiteness scan: first non-finite index of an array (atomicMin), used once
+// at upload so that pre-existing NaN/Inf in never-written slots are reported
+// like the reference's whole-store scan (modlc/interp.py:538-545).
+
+__global__ void k_first_nonfinite(const double* __restrict__ p, long long n,
+                                  unsigned long long* out) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; i < n; i += stride)
+    if (!isfinite(p[i])) atomicMin(out, (unsigned long long)i);
+}
+NMODL_API int nmodl_first_nonfinite(const double* p, long long n, unsigned long long* out_dev,
+                                    cudaStream_t s) {
+  if (n <= 0) return 0;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_first_nonfinite<<<blocks, 256, 0, s>>>(p, n, out_dev);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// deterministic checksums (fixed reduction tree, independent of launch
+// timing) for cross-rank validation: out[0] = sum(x), out[1] = sum(|x|).
+
+__global__ void k_checksum_partial(const double* __restrict__ p, long long n, double* part) {
+  __shared__ double s0[256], s1[256];
+  double a = 0.0, b = 0.0;
+  for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+    double x = p[i];
+    a += x;
+    b += fabs(x);
+  }
+  s0[threadIdx.x] = a;
+  s1[threadIdx.x] = b;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      s0[threadIdx.x] += s0[threadIdx.x + w];
+      s1[threadIdx.x] += s1[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = s0[0];
+    part[2 * blockIdx.x + 1] = s1[0];
+  }
+}
+__global__ void k_checksum_final(const double* part, int nb, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < nb; ++i) {
+      a += part[2 * i];
+      b += part[2 * i + 1];
+    }
+    out[0] = a;
+    out[1] = b;
+  }
+}
+NMODL_API int nmodl_checksum(const double* p, long long n, double* scratch_dev /* >= 2*1024 */,
+                             double* out_dev /* 2 */, cudaStream_t s) {
+  const int nb = 1024;
+  k_checksum_partial<<<nb, 256, 0, s>>>(p, n, scratch_dev);
+  k_checksum_final<<<1, 32, 0, s>>>(scratch_dev, nb, out_dev);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// L2 flush between timed iterations (write a buffer larger than L2).
+
+__global__ void k_fill(double* p, long long n, double v) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+NMODL_API int nmodl_l2_flush(double* buf, long long n_doubles, cudaStream_t s) {
+  k_fill<<<148 * 8, 256, 0, s>>>(buf, n_doubles, 0.0);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// node_index scatter layout (builder-defined extension; the reference has no
+// node arrays).  Stable counting sort of instances by node:
+//   counts[node]  = #instances on node
+//   offsets[0..N] = exclusive scan of counts
+//   perm[k]       = k-th instance in (node, instance) order   (stable)
+//   rank[i]       = position of instance i in that order (inverse of perm)
+// Stability is obtained without atomics-order dependence: every instance's
+// rank within its node is the number of equal-node instances before it,
+// computed per node segment after a histogram -- deterministic by
+// construction and bit-identical to np.argsort(node_index, kind="stable").
+
+__global__ void k_hist(const int* __restrict__ node_index, long long n, int n_nodes,
+                       unsigned int* counts, int* bad) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    int nd = node_index[i];
+    if (nd < 0 || nd >= n_nodes) {
+      atomicMin(bad, (int)(i < 0x7fffffff ? i : 0x7fffffff));
+      continue;
+    }
+    atomicAdd(&counts[nd], 1u);
+  }
+}
+
+// single-block exclusive scan over counts -> offsets (N+1 entries), chunked
+__global__ void k_scan(const unsigned int* counts, int n_nodes, long long* offsets) {
+  __shared__ long long s_carry;
+  __shared__ long long s_buf[1024];
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n_nodes; base += 1024) {
+    int i = base + threadIdx.x;
+    long long v = (i < n_nodes) ? (long long)counts[i] : 0;
+    s_buf[threadIdx.x] = v;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+      long long t = (threadIdx.x >= off) ? s_buf[threadIdx.x - off] : 0;
+      __syncthreads();
+      s_buf[threadIdx.x] += t;
+      __syncthreads();
+    }
+    if (i < n_nodes) offsets[i] = s_carry + s_buf[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) s_carry += s_buf[1023];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) offsets[n_nodes] = s_carry;
+}
+
+// Stable placement: CUB's LSD radix sort of (node, instance) pairs is stable,
+// so equal nodes keep ascending instance order -- bit-identical to
+// np.argsort(node_index, kind="stable").  Setup-time only.
+__global__ void k_iota_rank(long long* iota, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    iota[i] = i;
+}
+__global__ void k_invert(const long long* __restrict__ perm, long long* __restrict__ rank,
+                         long long n) {
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x)
+    rank[perm[k]] = k;
+}
+
+NMODL_API int nmodl_scatter_layout(const int* node_index_dev, long long n, int n_nodes,
+                                   unsigned int* counts_dev /* n_nodes */,
+                                   long long* offsets_dev /* n_nodes + 1 */,
+                                   long long* scratch_dev /* n */, long long* perm_dev /* n */,
+                                   long long* rank_dev /* n */, int* bad_dev /* 1 */,
+                                   cudaStream_t s) {
+  CK(cudaMemsetAsync(counts_dev, 0, sizeof(unsigned int) * (size_t)n_nodes, s));
+  int big = 0x7fffffff;
+  CK(cudaMemcpyAsync(bad_dev, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  k_hist<<<blocks, 256, 0, s>>>(node_index_dev, n, n_nodes, counts_dev, bad_dev);
+  k_scan<<<1, 1024, 0, s>>>(counts_dev, n_nodes, offsets_dev);
+  k_iota_rank<<<blocks, 256, 0, s>>>(scratch_dev, n);
+  int* keys_out = nullptr;
+  CK(cudaMallocAsync((void**)&keys_out, sizeof(int) * (size_t)(n > 0 ? n : 1), s));
+  int end_bit = 1;
+  while (end_bit < 31 && (1 << end_bit) < n_nodes) ++end_bit;
+  size_t temp_bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, node_index_dev, keys_out, scratch_dev,
+                                     perm_dev, (int64_t)n, 0, end_bit, s));
+  void* temp = nullptr;
+  CK(cudaMallocAsync(&temp, temp_bytes ? temp_bytes : 16, s));
+  CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, node_index_dev, keys_out, scratch_dev,
+                                     perm_dev, (int64_t)n, 0, end_bit, s));
+  k_invert<<<blocks, 256, 0, s>>>(perm_dev, rank_dev, n);
+  CK(cudaFreeAsync(temp, s));
+  CK(cudaFreeAsync(keys_out, s));
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+// gather/scatter of SoA arrays through a permutation (bind / download):
+//   dst[k] = src[perm[k]]   (gather, to node-sorted order)
+//   dst[perm[k]] = src[k]   (scatter back to instance order)
+__global__ void k_permute(const double* __restrict__ src, double* __restrict__ dst,
+                          const long long* __restrict__ perm, long long n, int inverse) {
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    long long j = perm[k];
+    if (inverse)
+      dst[j] = src[k];
+    else
+      dst[k] = src[j];
+  }
+}
+NMODL_API int nmodl_permute(const double* src, double* dst, const long long* perm, long long n,
+                            int inverse, cudaStream_t s) {
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  k_permute<<<blocks, 256, 0, s>>>(src, dst, perm, n, inverse);
+  CK(cudaGetLastError());
+  return 0;
+}
+__global__ void k_permute_i32(const int* __restrict__ src, int* __restrict__ dst,
+                              const long long* __restrict__ perm, long long n) {
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x)
+    dst[k] = src[perm[k]];
+}
+NMODL_API int nmodl_permute_i32(const int* src, int* dst, const long long* perm, long long n,
+                                cudaStream_t s) {
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  k_permute_i32<<<blocks, 256, 0, s>>>(src, dst, perm, n);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// v[i] = node_v[node_index[i]]  (materialise per-instance voltage on download)
+__global__ void k_gather_v(const double* __restrict__ node_v, const int* __restrict__ idx,
+                           double* __restrict__ v, long long n) {
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x)
+    v[k] = node_v[idx[k]];
+}
+NMODL_API int nmodl_gather_v(const double* node_v, const int* node_index, double* v, long long n,
+                             cudaStream_t s) {
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  k_gather_v<<<blocks, 256, 0, s>>>(node_v, node_index, v, n);
+  CK(cudaGetLastError());
+  return 0;
+}

@@ -1,0 +1,519 @@
+"""`CudaRunner`: the GPU drop-in for the reference's `interp.Runner`.
+
+Same constructor and `run_kernel(data, kernel_name, steps) -> data` contract
+as modlc/interp.py:124-131,456-471, operating in place on an `InstanceData`
+(the reference's, or any object with ``n/arrays/acc/scalars/newton_iters``),
+so `simulate`, `compare_pipelines` and `diff_trajectories`-style callers work
+unchanged.  Errors surface as `InterpError` with the reference's messages.
+
+Two ways to drive it:
+
+* host data (drop-in): every call uploads the store, runs the kernel(s) on the
+  device and writes the results back into the numpy arrays;
+* device-resident (`to_device` / `DeviceInstanceData`): the SoA store lives in
+  HBM across calls; `run_kernel` then only launches.  This is the production
+  path (and what `simulate` uses between its single upload and download).
+
+Kernel names are the reference's three plus ``"step"`` (fused
+state_update+current_update per timestep) and ``"step_nodes"`` (the
+node_index gather/scatter variant, see `bind_nodes`).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import sys
+
+import numpy as np
+
+from . import runtime as rt
+from .build import build_mechanism
+from .codegen_cuda import CudaOptions
+from .ir import NEWTON_MAX_ITER, from_layout, iter_nodes
+
+KERNELS = ("initialize", "state_update", "current_update", "step", "step_nodes")
+_PARTS = {
+    "initialize": ("initialize",),
+    "state_update": ("state_update",),
+    "current_update": ("current_update",),
+    "step": ("state_update", "current_update"),
+    "step_nodes": ("state_update", "current_update"),
+}
+_KNAME = {0: "initialize", 1: "state_update", 2: "current_update"}
+ALIGN = 256
+
+
+class InterpError(RuntimeError):
+    """Raised like the reference's modlc.interp.InterpError (interp.py:33-34)."""
+
+
+def _interp_error(msg: str) -> Exception:
+    """Return an exception that is also a modlc.interp.InterpError when the
+    reference runtime is loaded, so reference callers catch it unchanged."""
+    ref = sys.modules.get("modlc.interp")
+    if ref is not None and hasattr(ref, "InterpError"):
+        cls = type("InterpError", (InterpError, ref.InterpError), {})
+        return cls(msg)
+    return InterpError(msg)
+
+
+class HostInstanceData:
+    """Minimal InstanceData (modlc/interp.py:37-52) for callers without modlc."""
+
+    def __init__(self, n, arrays, acc, scalars, newton_iters=None):
+        self.n = n
+        self.arrays = arrays
+        self.acc = acc
+        self.scalars = scalars
+        self.newton_iters = list(newton_iters or [])
+
+    def copy(self):
+        return HostInstanceData(
+            self.n,
+            {k: v.copy() for k, v in self.arrays.items()},
+            {k: v.copy() for k, v in self.acc.items()},
+            dict(self.scalars),
+            list(self.newton_iters),
+        )
+
+
+class NodeBinding:
+    """node_index scatter layout resident on the device (builder extension).
+
+    perm/rank: node-stable sort of instances (np.argsort(node_index,
+    kind="stable") and its inverse); offsets: per-node instance segments in
+    sorted order; tile_nodes: CTA tiles made of whole node segments.
+    """
+
+    def __init__(self, n, n_nodes):
+        self.n = n
+        self.n_nodes = n_nodes
+        self.buffers = []
+
+    def alloc(self, nbytes):
+        b = rt.DeviceBuffer(nbytes)
+        self.buffers.append(b)
+        return b.ptr
+
+
+class DeviceInstanceData:
+    """Device-resident SoA store: one arena, 256-byte aligned arrays."""
+
+    def __init__(self, runner: "CudaRunner", n: int, names: list[str], scalars: dict):
+        self.runner = runner
+        self.n = n
+        self.names = list(names)  # data.arrays order (slots ..., v)
+        self.scalars = dict(scalars)
+        self.newton_iters: list[int] = []
+        stride = ((n * 8 + ALIGN - 1) // ALIGN) * ALIGN
+        self.stride = stride
+        count = len(self.names) + 2
+        self.arena = rt.DeviceBuffer(stride * count)
+        self.ptr = {name: self.arena.ptr + i * stride for i, name in enumerate(self.names)}
+        self.ptr["i_acc"] = self.arena.ptr + len(self.names) * stride
+        self.ptr["g_acc"] = self.arena.ptr + (len(self.names) + 1) * stride
+        nrw = max(1, len(runner.abi.rw_scalars))
+        self.scalars_rw = rt.DeviceBuffer(8 * nrw)
+        self.prebad: dict[str, int] = {}
+        self.nodes: NodeBinding | None = None
+
+    # ---- host <-> device ------------------------------------------------------
+    def upload_from(self, data, stream) -> None:
+        for name in self.names:
+            arr = np.ascontiguousarray(data.arrays[name], dtype=np.float64)
+            if arr.shape != (self.n,):
+                raise ValueError(f"array {name!r} has shape {arr.shape}, expected ({self.n},)")
+            rt.h2d(self.ptr[name], arr.ctypes.data, arr.nbytes, stream)
+            stream.sync() if arr is not data.arrays[name] else None
+        for name in ("i_acc", "g_acc"):
+            arr = np.ascontiguousarray(data.acc[name], dtype=np.float64)
+            rt.h2d(self.ptr[name], arr.ctypes.data, arr.nbytes, stream)
+        stream.sync()
+
+    def download_into(self, data, stream, names=None) -> None:
+        names = self.names if names is None else names
+        for name in names:
+            dst = data.arrays[name]
+            if not (dst.flags.c_contiguous and dst.dtype == np.float64):
+                tmp = np.empty(self.n)
+                rt.d2h(tmp.ctypes.data, self.ptr[name], tmp.nbytes, stream)
+                stream.sync()
+                dst[:] = tmp
+            else:
+                rt.d2h(dst.ctypes.data, self.ptr[name], dst.nbytes, stream)
+        for name in ("i_acc", "g_acc"):
+            dst = data.acc[name]
+            rt.d2h(dst.ctypes.data, self.ptr[name], dst.nbytes, stream)
+        stream.sync()
+
+    def array(self, name) -> np.ndarray:
+        out = np.empty(self.n)
+        s = self.runner.stream
+        rt.d2h(out.ctypes.data, self.ptr[name], out.nbytes, s)
+        s.sync()
+        return out
+
+
+class CudaRunner:
+    """Compiles one mechanism for sm_100a and executes its kernels."""
+
+    def __init__(self, layout, jac_mode: str = "exact", *, options: CudaOptions | None = None,
+                 fmad: bool = False, device: int = 0):
+        if jac_mode not in ("exact", "fd"):
+            raise ValueError("jac_mode must be 'exact' or 'fd'")
+        self.layout = layout
+        self.ir = from_layout(layout)
+        self.jac_mode = jac_mode
+        self.flags = 1 if jac_mode == "fd" else 0
+        rt.require_device(device)
+        self.device = device
+        self.options = options or CudaOptions()
+        self.mb = build_mechanism(self.ir, self.options, fmad)
+        self.abi = self.mb.abi
+        self.lib = C.CDLL(str(self.mb.so_path))
+        sym = self.mb.symbol
+        self.entry = {}
+        for k in KERNELS:
+            fn = getattr(self.lib, f"{sym}_{k}")
+            fn.restype = C.c_int
+            fn.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int]
+            self.entry[k] = fn
+        fields = []
+        for f in self.abi.fields:
+            ct = {"i64": C.c_longlong, "f64": C.c_double}.get(f.ctype, C.c_void_p)
+            fields.append((f.name, ct))
+        self.Struct = type(f"{sym}_data", (C.Structure,), {"_fields_": fields})
+        size_fn = getattr(self.lib, f"{sym}_abi_size")
+        size_fn.restype = C.c_longlong
+        if size_fn() != C.sizeof(self.Struct):
+            raise RuntimeError(f"ABI mismatch for {sym}: C {size_fn()} vs ctypes {C.sizeof(self.Struct)}")
+        self.stream = rt.Stream()
+        self.status = rt.DeviceBuffer(C.sizeof(rt.Status))
+        self._reset_status()
+        self.n_newton = len(self.abi.newton_nodes)
+        self._newton_kernel = [s.split(":")[0] for s in self.abi.newton_nodes]
+        self._max_iter = {}
+        for kname, stmts in self.ir.kernels.items():
+            for s in stmts:
+                for node in iter_nodes(s):
+                    if node.kind == "NewtonSolveNode":
+                        self._max_iter.setdefault(kname, int(node.attrs.get("max_iter", NEWTON_MAX_ITER)))
+
+    # ---- helpers ----------------------------------------------------------------
+    def _reset_status(self) -> None:
+        rt.check(rt.lib().nmodl_status_reset(C.c_void_p(self.status.ptr), C.c_void_p(self.stream.handle)),
+                 "status_reset")
+
+    def _read_status(self) -> rt.Status:
+        st = rt.Status()
+        rt.d2h(C.addressof(st), self.status.ptr, C.sizeof(st), self.stream)
+        self.stream.sync()
+        return st
+
+    def to_device(self, data) -> DeviceInstanceData:
+        """Upload an InstanceData into a device-resident store."""
+        names = list(data.arrays)
+        missing = [s for s in self.abi.slots if s not in data.arrays]
+        if missing or "v" not in data.arrays:
+            raise _interp_error(f"layout mismatch: instance data lacks {missing or ['v']}")
+        dev = DeviceInstanceData(self, int(data.n), names, data.scalars)
+        dev.newton_iters = list(data.newton_iters)
+        dev.upload_from(data, self.stream)
+        self._prescan(dev)
+        return dev
+
+    def _prescan(self, dev: DeviceInstanceData) -> None:
+        """First non-finite index per array, once per upload (interp.py:538-545)."""
+        buf = rt.DeviceBuffer(8 * len(dev.names))
+        rt.memset(buf.ptr, 0xFF, 8 * len(dev.names), self.stream)
+        L = rt.lib()
+        for i, name in enumerate(dev.names):
+            rt.check(L.nmodl_first_nonfinite(C.c_void_p(dev.ptr[name]), dev.n, C.c_void_p(buf.ptr + 8 * i),
+                                             C.c_void_p(self.stream.handle)), "first_nonfinite")
+        out = np.empty(len(dev.names), dtype=np.uint64)
+        rt.d2h(out.ctypes.data, buf.ptr, out.nbytes, self.stream)
+        self.stream.sync()
+        dev.prebad = {name: int(v) for name, v in zip(dev.names, out) if v != np.uint64(rt.NO_ERROR)}
+
+    def to_host(self, dev: DeviceInstanceData, data) -> None:
+        """Download a device store into `data` (arrays, acc, scalars, newton record)."""
+        if dev.nodes is not None:
+            self._unpermute_into(dev, data)
+        else:
+            dev.download_into(data, self.stream)
+        data.scalars.update(dev.scalars)
+        data.newton_iters[:] = dev.newton_iters
+
+    def _struct(self, dev: DeviceInstanceData, newton_rec=0):
+        md = self.Struct()
+        for f in self.abi.fields:
+            if f.role == "count":
+                setattr(md, f.name, dev.n)
+            elif f.role == "status":
+                setattr(md, f.name, self.status.ptr)
+            elif f.role == "newton":
+                setattr(md, f.name, newton_rec or None)
+            elif f.role == "scalars_rw":
+                setattr(md, f.name, dev.scalars_rw.ptr)
+            elif f.role == "scalar":
+                if f.key not in dev.scalars:
+                    raise _interp_error(f"unbound name {f.key!r}")
+                setattr(md, f.name, float(dev.scalars[f.key]))
+            elif f.role in ("v", "acc", "slot"):
+                setattr(md, f.name, dev.ptr[f.key])
+            elif f.role == "node":
+                nb = dev.nodes
+                if nb is None:
+                    setattr(md, f.name, 0 if f.ctype == "i64" else None)
+                else:
+                    setattr(md, f.name, getattr(nb, f.key))
+        return md
+
+    def _sync_scalars_in(self, dev) -> None:
+        rw = self.abi.rw_scalars
+        if rw:
+            vals = np.array([float(dev.scalars.get(s, 0.0)) for s in rw])
+            rt.h2d(dev.scalars_rw.ptr, vals.ctypes.data, vals.nbytes, self.stream)
+            self.stream.sync()
+
+    def _sync_scalars_out(self, dev) -> None:
+        rw = self.abi.rw_scalars
+        if rw:
+            vals = np.empty(len(rw))
+            rt.d2h(vals.ctypes.data, dev.scalars_rw.ptr, vals.nbytes, self.stream)
+            self.stream.sync()
+            for s, v in zip(rw, vals):
+                dev.scalars[s] = float(v)
+
+    # ---- execution -----------------------------------------------------------------
+    def launch(self, dev: DeviceInstanceData, kernel_name: str, steps: int = 1, newton_rec: int = 0) -> None:
+        """Enqueue `steps` launches on the runner's stream (no sync, no checks)."""
+        if kernel_name == "step_nodes" and dev.nodes is None:
+            raise ValueError("step_nodes needs bind_nodes() first")
+        md = self._struct(dev, newton_rec)
+        rc = self.entry[kernel_name](C.byref(md), int(steps), C.c_void_p(self.stream.handle), self.flags)
+        rt.check(rc, f"launch {self.mb.symbol}_{kernel_name}")
+
+    def run_kernel(self, data, kernel_name: str, steps: int = 1):
+        """modlc/interp.py:456-471 on the device."""
+        if kernel_name not in KERNELS:
+            raise KeyError(kernel_name)
+        host = not isinstance(data, DeviceInstanceData)
+        dev = self.to_device(data) if host else data
+        if steps > 0 and dev.n > 0:
+            self._run(dev, kernel_name, steps, host_data=data if host else None)
+        if host:
+            self.to_host(dev, data)
+        return data
+
+    def _run(self, dev, kernel_name, steps, host_data=None):
+        parts = _PARTS[kernel_name]
+        nn = self.n_newton
+        rec = None
+        if nn:
+            rec = rt.DeviceBuffer(4 * nn * steps)
+            rt.memset(rec.ptr, 0xFF, 4 * nn * steps, self.stream)
+        self._sync_scalars_in(dev)
+        self.launch(dev, kernel_name, steps, rec.ptr if rec else 0)
+        st = self._read_status()
+        self._sync_scalars_out(dev)
+        if rec is not None:
+            raw = np.empty(nn * steps, dtype=np.int32)
+            rt.d2h(raw.ctypes.data, rec.ptr, raw.nbytes, self.stream)
+            self.stream.sync()
+            raw = raw.reshape(steps, nn)
+            for step in range(steps):
+                for p in parts:
+                    for q in range(nn):
+                        if self._newton_kernel[q] == p and raw[step, q] >= 0:
+                            dev.newton_iters.append(int(raw[step, q]))
+        key = st.err_key
+        # pre-existing non-finite values in arrays this launch never rewrites
+        written = set(self.abi.kernels["step" if kernel_name == "step_nodes" else kernel_name]["stores"])
+        order = self.abi.array_order
+        kcode = {"initialize": 0, "state_update": 1, "current_update": 2}[parts[0]]
+        for name, idx in dev.prebad.items():
+            if name not in written and name in order:
+                cand = (kcode << 62) | (1 << 61) | (order.index(name) << 48) | idx
+                key = min(key, cand)
+        if key != rt.NO_ERROR:
+            self._reset_status()
+            if host_data is not None:
+                self.to_host(dev, host_data)
+            raise _interp_error(self._message(key, st, dev))
+
+    def _message(self, key, st, dev) -> str:
+        kernel = _KNAME[(key >> 62) & 3]
+        phase = (key >> 61) & 1
+        ordinal = (key >> 48) & 0x1FFF
+        kind = (key >> 46) & 3
+        inst = key & ((1 << 40) - 1)
+        if dev.nodes is not None:
+            inst = int(dev.nodes.perm_host[inst])
+        if phase == 1:
+            name = self.abi.array_order[ordinal]
+            return f"non-finite value in {name!r} at instance {inst} after kernel {kernel}"
+        if kind == 0:
+            return "WHILE loop exceeded 10000 iterations"
+        if kind == 1:
+            max_iter = self._max_iter.get(kernel, NEWTON_MAX_ITER)
+            return (f"Newton failed to converge for instance {inst} "
+                    f"(residual {st.payload:.3e} after {max_iter} iterations)")
+        return f"singular matrix in runtime linear solve (instance {inst})"
+
+    # ---- CUDA graphs -------------------------------------------------------------------
+    def capture(self, dev: DeviceInstanceData, kernel_name: str, steps: int) -> rt.Graph:
+        """Capture `steps` launches into a replayable graph (no Newton record)."""
+        self._sync_scalars_in(dev)
+        return rt.capture(self.stream, lambda: self.launch(dev, kernel_name, steps))
+
+    def check(self, dev: DeviceInstanceData, kernel_name: str = "step") -> None:
+        """Raise if any launch since the last check reported an error."""
+        st = self._read_status()
+        if st.err_key != rt.NO_ERROR:
+            self._reset_status()
+            raise _interp_error(self._message(st.err_key, st, dev))
+
+    # ---- node_index extension ----------------------------------------------------------
+    def bind_nodes(self, dev: DeviceInstanceData, node_index, node_v, node_rhs=None, node_d=None,
+                   tile: int | None = None) -> NodeBinding:
+        """Attach node arrays and reorder the store node-stably on the device."""
+        if dev.nodes is not None:
+            raise ValueError("nodes already bound")
+        node_index = np.ascontiguousarray(node_index, dtype=np.int32)
+        node_v = np.ascontiguousarray(node_v, dtype=np.float64)
+        n, n_nodes = dev.n, int(node_v.shape[0])
+        if node_index.shape != (n,):
+            raise ValueError("node_index must have one entry per instance")
+        nb = NodeBinding(n, n_nodes)
+        s = self.stream
+        L = rt.lib()
+        idx_in = nb.alloc(4 * n)
+        rt.h2d(idx_in, node_index.ctypes.data, 4 * n, s)
+        counts = nb.alloc(4 * n_nodes)
+        nb.node_offsets = nb.alloc(8 * (n_nodes + 1))
+        scratch = nb.alloc(8 * n)
+        nb.perm = nb.alloc(8 * n)
+        nb.rank = nb.alloc(8 * n)
+        bad = nb.alloc(4)
+        rt.check(L.nmodl_scatter_layout(C.c_void_p(idx_in), n, n_nodes, C.c_void_p(counts),
+                                        C.c_void_p(nb.node_offsets), C.c_void_p(scratch), C.c_void_p(nb.perm),
+                                        C.c_void_p(nb.rank), C.c_void_p(bad), C.c_void_p(s.handle)),
+                 "scatter_layout")
+        b = np.empty(1, dtype=np.int32)
+        rt.d2h(b.ctypes.data, bad, 4, s)
+        s.sync()
+        if b[0] != 0x7FFFFFFF:
+            raise ValueError(f"node_index out of range at instance {int(b[0])}")
+        nb.node_index = nb.alloc(4 * n)
+        rt.check(L.nmodl_permute_i32(C.c_void_p(idx_in), C.c_void_p(nb.node_index), C.c_void_p(nb.perm), n,
+                                     C.c_void_p(s.handle)), "permute_i32")
+        nb.node_v = nb.alloc(8 * n_nodes)
+        rt.h2d(nb.node_v, node_v.ctypes.data, 8 * n_nodes, s)
+        nb.node_rhs = nb.alloc(8 * n_nodes)
+        nb.node_d = nb.alloc(8 * n_nodes)
+        for ptr, host in ((nb.node_rhs, node_rhs), (nb.node_d, node_d)):
+            if host is None:
+                rt.memset(ptr, 0, 8 * n_nodes, s)
+            else:
+                h = np.ascontiguousarray(host, dtype=np.float64)
+                rt.h2d(ptr, h.ctypes.data, 8 * n_nodes, s)
+        # host copies of the (integer) layout for tiling and error remapping
+        offsets = np.empty(n_nodes + 1, dtype=np.int64)
+        rt.d2h(offsets.ctypes.data, nb.node_offsets, offsets.nbytes, s)
+        nb.perm_host = np.empty(n, dtype=np.int64)
+        rt.d2h(nb.perm_host.ctypes.data, nb.perm, nb.perm_host.nbytes, s)
+        s.sync()
+        nb.offsets_host = offsets
+        # target 3/4 of the shared-memory capacity so a tile rarely spills to
+        # the global-memory reduction path when a segment straddles a boundary
+        T = tile or max(1, (3 * self.options.tile) // 4)
+        tiles = tile_nodes_for(offsets, T)
+        nb.tile_nodes_host = tiles
+        nb.tile_nodes = nb.alloc(8 * len(tiles))
+        rt.h2d(nb.tile_nodes, tiles.ctypes.data, tiles.nbytes, s)
+        nb.n_tiles = len(tiles) - 1
+        # reorder every instance array into node-sorted order (on the device)
+        tmp = rt.DeviceBuffer(8 * n)
+        for name in list(dev.names) + ["i_acc", "g_acc"]:
+            rt.check(L.nmodl_permute(C.c_void_p(dev.ptr[name]), C.c_void_p(tmp.ptr), C.c_void_p(nb.perm), n, 0,
+                                     C.c_void_p(s.handle)), "permute")
+            rt.d2d(dev.ptr[name], tmp.ptr, 8 * n, s)
+        s.sync()
+        dev.nodes = nb
+        # prescan indices refer to instance order; remap to sorted positions
+        rank = np.empty(n, dtype=np.int64)
+        rt.d2h(rank.ctypes.data, nb.rank, rank.nbytes, s)
+        s.sync()
+        nb.rank_host = rank
+        dev.prebad = {k: int(rank[v]) for k, v in dev.prebad.items()}
+        return nb
+
+    def node_arrays(self, dev: DeviceInstanceData) -> dict:
+        nb = dev.nodes
+        out = {}
+        for name in ("node_rhs", "node_d", "node_v"):
+            arr = np.empty(nb.n_nodes)
+            rt.d2h(arr.ctypes.data, getattr(nb, name), arr.nbytes, self.stream)
+            out[name] = arr
+        for name, ptr, dt in (("perm", nb.perm, np.int64), ("rank", nb.rank, np.int64),
+                              ("node_index_sorted", nb.node_index, np.int32)):
+            arr = np.empty(nb.n, dtype=dt)
+            rt.d2h(arr.ctypes.data, ptr, arr.nbytes, self.stream)
+            out[name] = arr
+        offs = np.empty(nb.n_nodes + 1, dtype=np.int64)
+        rt.d2h(offs.ctypes.data, nb.node_offsets, offs.nbytes, self.stream)
+        out["offsets"] = offs
+        self.stream.sync()
+        return out
+
+    def _unpermute_into(self, dev, data) -> None:
+        nb = dev.nodes
+        L = rt.lib()
+        s = self.stream
+        tmp = rt.DeviceBuffer(8 * dev.n)
+        # per-instance voltage is the gathered node voltage
+        rt.check(L.nmodl_gather_v(C.c_void_p(nb.node_v), C.c_void_p(nb.node_index), C.c_void_p(dev.ptr["v"]),
+                                  dev.n, C.c_void_p(s.handle)), "gather_v")
+        for name in list(dev.names) + ["i_acc", "g_acc"]:
+            rt.check(L.nmodl_permute(C.c_void_p(dev.ptr[name]), C.c_void_p(tmp.ptr), C.c_void_p(nb.perm), dev.n, 1,
+                                     C.c_void_p(s.handle)), "unpermute")
+            dst = data.acc[name] if name in ("i_acc", "g_acc") else data.arrays[name]
+            rt.d2h(dst.ctypes.data, tmp.ptr, 8 * dev.n, s)
+            s.sync()
+
+
+def tile_nodes_for(offsets: np.ndarray, tile: int) -> np.ndarray:
+    """CTA tiles of whole node segments, ~`tile` instances each.
+
+    Boundary nodes are the first node whose segment starts at or after each
+    multiple of `tile`; a segment larger than a tile becomes its own tile
+    (the kernel then reduces it from global memory instead of shared).
+    """
+    n = int(offsets[-1])
+    n_nodes = len(offsets) - 1
+    if n_nodes == 0:
+        return np.zeros(1, dtype=np.int64)
+    marks = np.arange(0, max(n, 1), tile, dtype=np.int64)
+    starts = np.searchsorted(offsets[:-1], marks, side="left")
+    bounds = np.unique(np.concatenate([[0], starts, [n_nodes]])).astype(np.int64)
+    return bounds
+
+
+def simulate(layout, data, steps: int, jac_mode: str = "exact", on_step=None, runner: CudaRunner | None = None):
+    """GPU twin of modlc.interp.simulate (interp.py:640-655): one upload,
+    initialize, `steps` fused state+current launches, one download."""
+    runner = runner or CudaRunner(layout, jac_mode=jac_mode)
+    dev = runner.to_device(data)
+    try:
+        runner.run_kernel(dev, "initialize", 1)
+        if on_step is None:
+            runner.run_kernel(dev, "step", steps)
+        else:
+            for step in range(steps):
+                runner.run_kernel(dev, "step", 1)
+                runner.to_host(dev, data)
+                on_step(step, data)
+    finally:
+        runner.to_host(dev, data)
+    return data

@@ -1,0 +1,46 @@
+"""Parity metrics shared by the GPU tests.
+
+`rel_dev` is the reference's diff_trajectories metric (modlc/interp.py:658-672):
+max |a-b| / max(|a|, |b|, 1e-30).  `rel_dev_floor` adds the per-slot scale
+floor BASELINE.md §4 motivates for CONSERVE/LU schemes: the denominator is
+at least floor * max|slot|, so 1e-14-magnitude occupancies do not turn ulp
+noise of the exp() implementations into large relative errors.
+"""
+
+import numpy as np
+
+TOL = 1e-10  # north star: 1e-10 relative in fp64 after 1000 timesteps
+
+
+def _pair(a, b, name):
+    xa = a.acc[name] if name in a.acc else a.arrays[name]
+    xb = b.acc[name] if name in b.acc else b.arrays[name]
+    return np.asarray(xa), np.asarray(xb)
+
+
+def rel_dev(a, b, names):
+    worst, where = 0.0, None
+    for name in names:
+        xa, xb = _pair(a, b, name)
+        d = np.abs(xa - xb) / np.maximum(np.maximum(np.abs(xa), np.abs(xb)), 1e-30)
+        m = float(np.max(d)) if d.size else 0.0
+        if m > worst:
+            worst, where = m, name
+    return worst, where
+
+
+def rel_dev_floor(a, b, names, floor=1e-6):
+    worst, where = 0.0, None
+    for name in names:
+        xa, xb = _pair(a, b, name)
+        scale = max(float(np.max(np.abs(xa))) if xa.size else 0.0, float(np.max(np.abs(xb))) if xb.size else 0.0)
+        den = np.maximum(np.maximum(np.maximum(np.abs(xa), np.abs(xb)), floor * scale), 1e-30)
+        m = float(np.max(np.abs(xa - xb) / den)) if xa.size else 0.0
+        if m > worst:
+            worst, where = m, name
+    return worst, where
+
+
+def compared_names(ir):
+    """States, ion variables, every other slot, and the accumulators."""
+    return list(ir.slot_names()) + ["v", "i_acc", "g_acc"]

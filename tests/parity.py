@@ -44,3 +44,32 @@ def rel_dev_floor(a, b, names, floor=1e-6):
 def compared_names(ir):
     """States, ion variables, every other slot, and the accumulators."""
     return list(ir.slot_names()) + ["v", "i_acc", "g_acc"]
+
+
+H = 0.001  # CONDUCTANCE_PERTURBATION, modlc/odes.py:45
+
+
+def g_acc_dev(ir, a, b):
+    """Numeric-conductance g_acc is a difference quotient (i(v+h) - i(v))/h
+    (modlc/interp.py:495-514): its rounding error scales with |i|/h, not |g|.
+    The reference's own two CPU paths (numpy oracle vs emitted C) disagree by
+    8.6e-10 pure-relative on it (ProbAMPANMDA_EMS, 1000 steps).  We therefore
+    hold it to the north-star 1e-10 relative to the currents it is built from:
+    |dg| <= 1e-10 * max(|g|, |i_acc|/h)."""
+    ga, gb = np.asarray(a.acc["g_acc"]), np.asarray(b.acc["g_acc"])
+    ia = np.abs(np.asarray(a.acc["i_acc"]))
+    den = np.maximum(np.maximum(np.maximum(np.abs(ga), np.abs(gb)), ia / H), 1e-30)
+    return float(np.max(np.abs(ga - gb) / den)) if ga.size else 0.0
+
+
+def parity(ir, a, b, floored=False):
+    """(worst deviation, slot) using the metric appropriate to each slot."""
+    names = compared_names(ir)
+    numeric_g = bool(ir.currents) and not ir.analytic_conductance
+    plain = [x for x in names if not (numeric_g and x == "g_acc")]
+    worst, where = (rel_dev_floor(a, b, plain) if floored else rel_dev(a, b, plain))
+    if numeric_g:
+        g = g_acc_dev(ir, a, b)
+        if g > worst:
+            worst, where = g, "g_acc"
+    return worst, where

@@ -1,0 +1,580 @@
+"""Benchmark: nrn_state + nrn_cur instance-steps/s (fp64) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload synapse10m|hh1m|bbp20m|kinetic1m] [--no-also]
+
+One JSON line on rank 0.  A "step" is one timestep of the hot path over the
+whole synthetic population on every rank: one fused nrn_state+nrn_cur launch
+per mechanism (for the default workload also the node_index gather and the
+in-order rhs/d reduction, inside the same kernel).  Workloads are the
+BASELINE.json configs:
+
+  synapse10m  configs[1]  ProbAMPANMDA_EMS restated (4 cnexp states, Mg block,
+                          numeric conductance), 10M instances / GPU, random
+                          node_index onto 1M nodes (default; inputs >> L2)
+  hh1m        configs[0]  hh (cnexp, analytic conductance), 1M instances / GPU
+                          (working set ~ L2: L2 flushed between timed steps)
+  bbp20m      configs[2]  NaTs2_t, K_Pst, Ca_HVA, SKv3_1, Ih, CaDynamics_E2;
+                          20M instances / GPU split evenly (6 launches / step)
+  kinetic1m   configs[3]  6-state KINETIC Na (runtime LU k=6) + cdp5-style
+                          Newton k=5 with LU, 1M instances each
+
+Multi-GPU (torchrun): one process per GPU, each rank owns its own shard of
+cells (weak scaling, no per-step collective); timings are CUDA events on the
+launching stream, max over ranks; NCCL only all-reduces validation checksums.
+`--impl reference` times the reference's own CPU implementation (its emitted
+scalar C, oracle/_ref, compiled -O3 -march=native, all host threads) on a
+bounded sample of the same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BASELINE = json.loads((ROOT / "BASELINE.json").read_text())
+METRIC = BASELINE["metric"]
+UNIT = "instance-steps/s"
+
+WORKLOADS = {
+    "synapse10m": {
+        "config": BASELINE["configs"][1],
+        "mechs": [("ProbAMPANMDA_EMS", 10_000_000)],
+        "nodes": 1_000_000,
+    },
+    "hh1m": {"config": BASELINE["configs"][0], "mechs": [("hh_subset", 1_000_000)], "nodes": 0},
+    "bbp20m": {
+        "config": BASELINE["configs"][2],
+        "mechs": [(m, 20_000_000 // 6) for m in ("NaTs2_t", "K_Pst", "Ca_HVA", "SKv3_1", "Ih", "cadyn")],
+        "nodes": 0,
+    },
+    "kinetic1m": {"config": BASELINE["configs"][3], "mechs": [("na6", 1_000_000), ("cdp5ish", 1_000_000)], "nodes": 0},
+}
+DEFAULT_WORKLOAD = "synapse10m"
+
+
+def bench_options():
+    from paper_1905_02241_b200.codegen_cuda import CudaOptions
+
+    return {"direct": CudaOptions(ilp=2), "nodes": CudaOptions()}
+
+
+def bench_irs():
+    """(IR, options) pairs bench.py launches -- prebuilt by __graft_entry__.build()."""
+    from paper_1905_02241_b200.ir import MechIR
+
+    opts = bench_options()
+    out = []
+    for w in WORKLOADS.values():
+        for stem, _ in w["mechs"]:
+            ir = MechIR.load(ROOT / "fixtures" / "ir" / f"{stem}.json")
+            out.append((ir, opts["nodes"] if w["nodes"] else opts["direct"]))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for name, val in zip(names, r[5:9]):
+                if val.strip().lower() == "active":
+                    reasons.add(name)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(mx) if mx else None,
+            "reasons": sorted(reasons),
+            "samples": len(self.rows),
+        }
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def allreduce(self, values, op="max"):
+        if not self.pg:
+            return list(values)
+        import torch
+
+        t = torch.tensor(list(values), dtype=torch.float64, device=f"cuda:{self.local}")
+        self.pg.all_reduce(t, op={"max": self.pg.ReduceOp.MAX, "sum": self.pg.ReduceOp.SUM}[op])
+        return t.cpu().tolist()
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# our implementation
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.is_file():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _ncu_traffic(workload):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.is_file():
+        d = json.loads(p.read_text())
+        return d.get(workload)
+    return None
+
+
+class Population:
+    """One mechanism population resident on this GPU."""
+
+    def __init__(self, stem, n, n_nodes, seed, options):
+        from paper_1905_02241_b200.instance import init, node_layout
+        from paper_1905_02241_b200.ir import MechIR
+        from paper_1905_02241_b200.runner import CudaRunner
+
+        self.stem = stem
+        self.ir = MechIR.load(ROOT / "fixtures" / "ir" / f"{stem}.json")
+        self.n = n
+        self.n_nodes = n_nodes
+        self.runner = CudaRunner(self.ir, options=options)
+        self.data = init(self.ir, n, seed)
+        self.kernel = "step_nodes" if n_nodes else "step"
+        if n_nodes:
+            self.node_index, self.node_v = node_layout(n, n_nodes, seed)
+        self.dev = None
+
+    def setup_device(self):
+        import ctypes as C
+
+        from paper_1905_02241_b200 import runtime as rt
+
+        r = self.runner
+        self.dev = r.to_device(self.data)
+        if self.n_nodes:
+            nb = r.bind_nodes(self.dev, self.node_index, self.node_v)
+            rt.check(rt.lib().nmodl_gather_v(C.c_void_p(nb.node_v), C.c_void_p(nb.node_index),
+                                             C.c_void_p(self.dev.ptr["v"]), self.n, C.c_void_p(r.stream.handle)),
+                     "gather_v")
+        r.run_kernel(self.dev, "initialize", 1)
+
+    def launch(self, steps=1):
+        self.runner.launch(self.dev, self.kernel, steps)
+
+    def launch_bytes(self):
+        from paper_1905_02241_b200.traffic import launch_bytes
+
+        return launch_bytes(self.runner.abi, self.n, self.kernel, self.n_nodes)
+
+
+def run_workload(name, args, dist, stream_timing=True):
+    from paper_1905_02241_b200 import runtime as rt
+
+    w = WORKLOADS[name]
+    opts = bench_options()
+    seed = 42 + dist.rank
+    pops = [Population(stem, n, w["nodes"], seed, opts["nodes"] if w["nodes"] else opts["direct"])
+            for stem, n in w["mechs"]]
+    for p in pops:
+        p.setup_device()
+    info = rt.device_info(dist.local)
+    streams = [p.runner.stream for p in pops]
+    working = sum(p.launch_bytes() for p in pops)
+    flush = working < 3 * info["l2_bytes"]
+    flush_buf = rt.DeviceBuffer(2 * info["l2_bytes"]) if flush else None
+    s0 = streams[0]
+    # all populations on one stream so the step sequence is ordered
+    for p in pops:
+        p.runner.stream = s0
+    ev_a, ev_b = rt.Event(), rt.Event()
+    K, W = args.steps, args.warmup
+    for _ in range(W):
+        for p in pops:
+            p.launch(1)
+    s0.sync()
+    for p in pops:
+        p.runner.check(p.dev)
+    # per-kernel timing (launch duration of the dominant kernel) + step time
+    per_pop_ms = [0.0] * len(pops)
+    evs = [(rt.Event(), rt.Event()) for _ in pops]
+    dist.barrier()
+    s0.sync()
+    total_ms = 0.0
+    visible = os.environ.get("CUDA_VISIBLE_DEVICES")
+    phys = int(visible.split(",")[dist.local]) if visible and visible.split(",")[0].isdigit() else dist.local
+    with ClockSampler(phys) as clk:
+        if flush:
+            for _ in range(K):
+                rt.check(rt.lib().nmodl_l2_flush(C_void(flush_buf.ptr), flush_buf.nbytes // 8, C_void(s0.handle)), "flush")
+                ev_a.record(s0)
+                for j, p in enumerate(pops):
+                    evs[j][0].record(s0)
+                    p.launch(1)
+                    evs[j][1].record(s0)
+                ev_b.record(s0)
+                ev_b.sync()
+                total_ms += ev_a.elapsed_ms(ev_b)
+                for j in range(len(pops)):
+                    per_pop_ms[j] += evs[j][0].elapsed_ms(evs[j][1])
+        else:
+            graph = rt.capture(s0, lambda: [p.launch(1) for _ in range(K) for p in pops])
+            ev_a.record(s0)
+            graph.launch(s0)
+            ev_b.record(s0)
+            ev_b.sync()
+            total_ms = ev_a.elapsed_ms(ev_b)
+            # separate pass: per-population launch durations (same stream, events between kernels)
+            for _ in range(min(K, 10)):
+                for j, p in enumerate(pops):
+                    evs[j][0].record(s0)
+                    p.launch(1)
+                    evs[j][1].record(s0)
+                s0.sync()
+                for j in range(len(pops)):
+                    per_pop_ms[j] += evs[j][0].elapsed_ms(evs[j][1]) * (K / min(K, 10))
+    s0.sync()
+    for p in pops:
+        p.runner.check(p.dev)
+    clocks = clk.summary()
+    dist.barrier()
+    max_ms = dist.allreduce([total_ms], "max")[0]
+    n_rank = sum(p.n for p in pops)
+    n_all = dist.allreduce([float(n_rank)], "sum")[0]
+    value = n_all * K / (max_ms / 1e3)
+    # roofline of the dominant kernel (largest share of the step)
+    j = int(np.argmax(per_pop_ms))
+    dom = pops[j]
+    dom_ms = per_pop_ms[j] / K
+    peak, peak_src = _peaks()
+    achieved = dom.launch_bytes() / (dom_ms / 1e3) / 1e9
+    from paper_1905_02241_b200.traffic import describe
+
+    res = {
+        "value": value,
+        "ms_per_step": max_ms / K,
+        "n_rank": n_rank,
+        "clocks": clocks,
+        "gpu_launches": K * len(pops),
+        "l2": "L2 flushed between timed steps" if flush else "inputs larger than L2 (no flush)",
+        "roofline": {
+            "bound": "hbm",
+            "kernel": f"{dom.runner.mb.symbol}_k_{dom.kernel}",
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": achieved / peak,
+            "traffic": _ncu_traffic(name),
+            "peak_source": peak_src,
+            "bytes_per_launch": dom.launch_bytes(),
+            "model": describe(dom.runner.abi, dom.kernel),
+            "share_of_step": per_pop_ms[j] / max(sum(per_pop_ms), 1e-30),
+            "launch_ms": dom_ms,
+        },
+        "per_mechanism": {
+            p.stem: {"instances": p.n, "ms_per_launch": per_pop_ms[i] / K,
+                     "GBps": p.launch_bytes() / (per_pop_ms[i] / K / 1e3) / 1e9,
+                     "bytes_per_instance_step": p.launch_bytes() / p.n}
+            for i, p in enumerate(pops)
+        },
+        "pops": pops,
+    }
+    return res
+
+
+def C_void(x):
+    import ctypes
+
+    return ctypes.c_void_p(x)
+
+
+def e2e_measure(name, dist, calls=2, timesteps=1000):
+    """Same metric through the public API with host buffers: each call uploads
+    the population from pinned host memory, binds nodes, runs nrn_init and
+    `timesteps` fused steps, and downloads the full store (and node arrays)."""
+    from paper_1905_02241_b200 import runtime as rt
+    from paper_1905_02241_b200.instance import init, node_layout
+    from paper_1905_02241_b200.ir import MechIR
+    from paper_1905_02241_b200.runner import CudaRunner, simulate, simulate_nodes
+
+    w = WORKLOADS[name]
+    opts = bench_options()
+    seed = 42 + dist.rank
+    jobs = []
+    for stem, n in w["mechs"]:
+        ir = MechIR.load(ROOT / "fixtures" / "ir" / f"{stem}.json")
+        runner = CudaRunner(ir, options=opts["nodes"] if w["nodes"] else opts["direct"])
+        data = init(ir, n, seed)
+        pins = [rt.PinnedRegistration(a) for a in list(data.arrays.values()) + list(data.acc.values())]
+        extra = None
+        if w["nodes"]:
+            idx, nv = node_layout(n, w["nodes"], seed)
+            extra = (idx, nv)
+            pins += [rt.PinnedRegistration(idx), rt.PinnedRegistration(nv)]
+        jobs.append((ir, runner, data, extra, pins, n))
+
+    def one_call():
+        for ir, runner, data, extra, _, n in jobs:
+            if extra is None:
+                simulate(ir, data, timesteps, runner=runner)
+            else:
+                simulate_nodes(ir, data, timesteps, extra[0], extra[1], runner=runner)
+
+    one_call()  # warm-up (also primes graph/occupancy caches)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(calls):
+        one_call()
+    dt = time.perf_counter() - t0
+    dt = dist.allreduce([dt], "max")[0]
+    n_all = dist.allreduce([float(sum(j[5] for j in jobs))], "sum")[0]
+    return {
+        "value": n_all * timesteps * calls / dt,
+        "unit": UNIT,
+        "h2d_bytes_per_step": int(sum(_h2d(j) for j in jobs)),
+        "d2h_bytes_per_step": int(sum(_d2h(j) for j in jobs)),
+        "step": f"one public-API call: pinned H2D of the store, nrn_init, {timesteps} timesteps, D2H of the store"
+                + (", node_index upload + device sort, node rhs/d download" if w["nodes"] else ""),
+        "timesteps_per_call": timesteps,
+        "calls": calls,
+    }
+
+
+def _h2d(job):
+    ir, runner, data, extra, _, n = job
+    b = sum(a.nbytes for a in data.arrays.values()) + sum(a.nbytes for a in data.acc.values())
+    if extra is not None:
+        b += extra[0].nbytes + extra[1].nbytes
+    return b
+
+
+def _d2h(job):
+    ir, runner, data, extra, _, n = job
+    b = sum(a.nbytes for a in data.arrays.values()) + sum(a.nbytes for a in data.acc.values())
+    if extra is not None:
+        b += 3 * extra[1].nbytes + 2 * 8 * n + 4 * n
+    return b
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (the reference's emitted C, all host threads)
+
+
+def cpu_reference(name, target_s=10.0, max_n=2_000_000, steps_cap=200):
+    from oracle import ref_c
+    from paper_1905_02241_b200.instance import init
+    from paper_1905_02241_b200.ir import MechIR
+
+    w = WORKLOADS[name]
+    threads = os.cpu_count() or 1
+    per_mech = []
+    total_inst_steps = 0.0
+    total_s = 0.0
+    for stem, n in w["mechs"]:
+        if not ref_c.available(stem):
+            return None
+        so = ref_c.native_build(stem)
+        r = ref_c.RefC(stem, so)
+        ir = MechIR.load(ROOT / "fixtures" / "ir" / f"{stem}.json")
+        ns = min(n, max_n)
+        data = init(ir, ns, 42)
+        r.initialize(data)
+        t0 = time.perf_counter()
+        r.steps(data, 2, threads)
+        dt1 = (time.perf_counter() - t0) / 2
+        steps = int(max(2, min(steps_cap, (target_s / len(w["mechs"])) / max(dt1, 1e-6))))
+        t0 = time.perf_counter()
+        r.steps(data, steps, threads)
+        dt = time.perf_counter() - t0
+        per_mech.append(f"{stem}: {ns} instances x {steps} steps in {dt:.2f}s")
+        # time-weighted combination: the population's full step is the sum of its mechanisms
+        total_s += dt * (n / ns) / steps
+        total_inst_steps += n
+    value = total_inst_steps / total_s
+    return {
+        "value": value,
+        "unit": UNIT,
+        "cores": threads,
+        "kind": "reference",
+        "sample": "reference-emitted scalar C (modlc.codegen.emit_scalar, count field renamed), gcc -O3 "
+                  "-march=native, contiguous shards per thread, accumulators zeroed per step; "
+                  + "; ".join(per_mech)
+                  + ("; no node_index scatter (the reference has none)" if w["nodes"] else ""),
+        "cpu": _cpu_model(),
+    }
+
+
+def _cpu_model():
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=list(WORKLOADS), default=DEFAULT_WORKLOAD)
+    ap.add_argument("--no-also", action="store_true", help="skip the secondary workloads")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    dist = Dist()
+    w = WORKLOADS[args.workload]
+    config = {
+        "workload": args.workload,
+        "baseline_config": w["config"],
+        "mechanisms": {stem: n for stem, n in w["mechs"]},
+        "instances_per_gpu": sum(n for _, n in w["mechs"]),
+        "n_nodes_per_gpu": w["nodes"],
+        "dt_ms": 0.025,
+        "parallelism": f"{args.gpus} x instance shard by cell (weak scaling, no per-step collective)",
+    }
+    if args.impl == "reference":
+        if dist.rank == 0:
+            K, W = args.steps, args.warmup
+            ref = cpu_reference(args.workload, target_s=max(2.0, 20.0 / max(K + W, 1)))
+            line = {"impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": args.gpus, "steps": K,
+                    "warmup": W, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                    "data": "synthetic (modlc.interp.init-format seeded instance store)", "config": config}
+            if ref is None:
+                line.update({"unavailable": "oracle/_ref not built (needs the reference front-end)"})
+            else:
+                line.update({"value": ref["value"], "ms_per_step": None,
+                             "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu")},
+                             "e2e": {"value": ref["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+            print(json.dumps(line), flush=True)
+        dist.close()
+        return
+    from paper_1905_02241_b200 import runtime as rt
+
+    rt.require_device(dist.local)
+    res = run_workload(args.workload, args, dist)
+    e2e = None if args.no_e2e else e2e_measure(args.workload, dist)
+    also = {}
+    if not args.no_also:
+        for other in ("hh1m", "bbp20m", "kinetic1m"):
+            if other == args.workload:
+                continue
+            a = argparse.Namespace(steps=min(args.steps, 20), warmup=3)
+            r = run_workload(other, a, dist)
+            also[other] = {"value": r["value"], "ms_per_step": r["ms_per_step"], "l2": r["l2"],
+                           "roofline": {k: r["roofline"][k] for k in ("kernel", "achieved", "peak", "frac", "bytes_per_launch", "launch_ms")},
+                           "per_mechanism": r["per_mechanism"]}
+            del r
+    cpu = None
+    if dist.rank == 0 and args.gpus == 1:
+        cpu = cpu_reference(args.workload)
+    if dist.rank == 0:
+        config["l2_policy"] = res["l2"]
+        line = {
+            "metric": METRIC,
+            "value": res["value"],
+            "unit": UNIT,
+            "n_gpus": args.gpus,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": res["ms_per_step"],
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (modlc.interp.init-format seeded instance store; random node_index)",
+            "config": config,
+            "roofline": res["roofline"],
+            "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu")},
+            "e2e": e2e,
+            "gpu_launches": res["gpu_launches"],
+            "clocks": res["clocks"],
+            "per_mechanism": res["per_mechanism"],
+            "also": also,
+        }
+        print(json.dumps(line), flush=True)
+    dist.close()
+
+
+if __name__ == "__main__":
+    main()

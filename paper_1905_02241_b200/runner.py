@@ -517,3 +517,28 @@ def simulate(layout, data, steps: int, jac_mode: str = "exact", on_step=None, ru
     finally:
         runner.to_host(dev, data)
     return data
+
+
+def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, node_d=None,
+                   jac_mode: str = "exact", runner: CudaRunner | None = None):
+    """node_index run of one mechanism population (builder extension).
+
+    Per timestep: v_i = node_v[node_index[i]]; nrn_state; nrn_cur; then
+    node_rhs[k] -= sum_i i_acc[i] and node_d[k] += sum_i g_acc[i] over the
+    instances i of node k in ascending instance order (deterministic; the
+    oracle restatement is oracle/nodes_np.py).  Instances are initialised
+    with the gathered voltage.  Returns (data, node_rhs, node_d); `data` is
+    updated in place in instance order.
+    """
+    runner = runner or CudaRunner(layout, jac_mode=jac_mode)
+    dev = runner.to_device(data)
+    nb = runner.bind_nodes(dev, node_index, node_v, node_rhs, node_d)
+    rt.check(rt.lib().nmodl_gather_v(C.c_void_p(nb.node_v), C.c_void_p(nb.node_index), C.c_void_p(dev.ptr["v"]),
+                                     dev.n, C.c_void_p(runner.stream.handle)), "gather_v")
+    try:
+        runner.run_kernel(dev, "initialize", 1)
+        runner.run_kernel(dev, "step_nodes", steps)
+    finally:
+        runner.to_host(dev, data)
+    out = runner.node_arrays(dev)
+    return data, out["node_rhs"], out["node_d"]

@@ -1,0 +1,212 @@
+"""CPU-side tests of the product: printer, IR, ABI, C-ABI exports, host logic.
+
+No CUDA device needed: libraries are loaded with ctypes and only host-side
+functions (ABI descriptors) are called.
+"""
+
+import ctypes
+import json
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, all_ir_stems, load_ir
+from paper_1905_02241_b200.codegen_cuda import (
+    CudaOptions,
+    CudaPrinter,
+    UnsupportedConstruct,
+    emit_cuda,
+    emit_cuda_header,
+)
+from paper_1905_02241_b200.ir import MechIR, Node, Slot
+
+
+def test_emission_deterministic_and_named():
+    """Same contract as the reference emitters (pkg/tests/test_codegen.py:9-23)."""
+    ir = load_ir("corpus_cat")
+    a, b = emit_cuda(ir), emit_cuda(load_ir("corpus_cat"))
+    assert a.text == b.text
+    assert a.backend == "cuda" and a.filename == "cat.cu"
+    assert "__global__" in a.text and "cat_k_step" in a.text
+    assert 'extern "C"' in a.text
+
+
+@pytest.mark.parametrize("stem", all_ir_stems())
+def test_every_fixture_prints(stem):
+    text = emit_cuda(load_ir(stem)).text
+    assert text.endswith("\n")
+
+
+def test_abi_field_order_mirrors_reference_struct():
+    """count, scalars (sorted), v, i_acc, g_acc, slots in layout order
+    (modlc/codegen.py:425-437), count renamed, extension fields appended."""
+    ir = load_ir("hh_subset")
+    p = CudaPrinter(ir)
+    p.emit_unit()
+    names = [f.name for f in p._abi.fields]
+    assert names[0] == "n_instances"
+    scal = [f.name for f in p._abi.fields if f.role == "scalar"]
+    assert scal == sorted(ir.global_scalars)
+    i_v = names.index("v")
+    assert names[i_v : i_v + 3] == ["v", "i_acc", "g_acc"]
+    slots = [f.key for f in p._abi.fields if f.role == "slot"]
+    assert slots == ir.slot_names()
+    assert "n" in slots  # STATE n no longer collides with the count field
+
+
+def test_traffic_model_hh_is_144_bytes():
+    """hh fused unique traffic = 10 reads + 8 writes = 144 B."""
+    from paper_1905_02241_b200.traffic import bytes_per_instance
+
+    p = CudaPrinter(load_ir("hh_subset"))
+    p.emit_unit()
+    k = p._abi.kernels["step"]
+    assert sorted(k["loads"]) == sorted(["gnabar", "gkbar", "gl", "el", "m", "h", "n", "ena", "ek", "v"])
+    assert sorted(k["stores"]) == sorted(["ina", "ik", "il", "m", "h", "n"])
+    assert bytes_per_instance(p._abi, "step") == 144
+
+
+def test_verbatim_in_kernel_is_rejected():
+    ir = load_ir("corpus_leak")
+    ir.kernels["state_update"] = (Node("Verbatim", (), {"text": "x = 1;"}),)
+    with pytest.raises(UnsupportedConstruct):
+        emit_cuda(ir)
+
+
+def test_per_lane_global_write_is_rejected():
+    """Last-active-lane GLOBAL writes (modlc/interp.py:361-367) are not lowered."""
+    ir = load_ir("corpus_globals2")
+    ident = lambda n: Node("Identifier", (), {"name": n})
+    ir.kernels["state_update"] = ir.kernels["state_update"] + (Node("Assign", (ident("tadj"), ident("v"))),)
+    with pytest.raises(UnsupportedConstruct):
+        emit_cuda(ir)
+
+
+def test_uniform_global_write_is_lowered():
+    text = emit_cuda(load_ir("corpus_globals2")).text
+    assert "scalars_rw" in text and "g_tadj" in text
+
+
+def test_ir_json_round_trip():
+    ir = load_ir("cdp5ish")
+    again = MechIR.from_json(ir.to_json())
+    assert again.to_json() == ir.to_json()
+    assert emit_cuda(again).text == emit_cuda(ir).text
+
+
+def test_ir_matches_reference_front_end_when_available():
+    from paper_1905_02241_b200 import frontend
+
+    if not frontend.modlc_available():
+        pytest.skip("reference front-end not importable here")
+    fresh = frontend.compile_mod(ROOT / "fixtures" / "mod" / "hh_subset.mod")
+    fresh.meta = load_ir("hh_subset").meta
+    assert fresh.to_obj()["kernels"] == load_ir("hh_subset").to_obj()["kernels"]
+
+
+def test_headers_up_to_date():
+    for h in sorted((ROOT / "include" / "mechanisms").glob("*.h")):
+        mech = h.stem
+        stem = next(s for s in all_ir_stems() if load_ir(s).mechanism == mech and "." not in s)
+        assert emit_cuda_header(load_ir(stem)).text == h.read_text(), h.name
+
+
+# ---- C-ABI exports ---------------------------------------------------------------
+
+
+def _declared(header: Path):
+    text = header.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    text = re.sub(r"#define NMODL_B200_MECHANISM.*?\n\n", "\n", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(nmodl_\w+)\s*\(", text)))
+
+
+def test_runtime_library_exports_every_declared_symbol():
+    from paper_1905_02241_b200.build import build_runtime
+    from paper_1905_02241_b200.runtime import RUNTIME_SYMBOLS
+
+    lib = ctypes.CDLL(str(build_runtime()))
+    declared = _declared(ROOT / "include" / "nmodl_b200.h")
+    assert declared, "no declarations parsed"
+    for sym in declared:
+        assert hasattr(lib, sym), sym
+    assert set(RUNTIME_SYMBOLS) <= set(declared)
+    lib.nmodl_abi_version.restype = ctypes.c_int
+    assert lib.nmodl_abi_version() == 1
+    lib.nmodl_status_size.restype = ctypes.c_int
+    assert lib.nmodl_status_size() == 32
+
+
+@pytest.mark.parametrize("stem", ["hh_subset", "ProbAMPANMDA_EMS", "na6", "cdp5ish", "corpus_cat"])
+def test_mechanism_library_exports_and_abi(stem):
+    from paper_1905_02241_b200.build import build_mechanism
+
+    ir = load_ir(stem)
+    mb = build_mechanism(ir)
+    lib = ctypes.CDLL(str(mb.so_path))
+    for k in ("initialize", "state_update", "current_update", "step", "step_nodes", "abi", "abi_size"):
+        assert hasattr(lib, f"{mb.symbol}_{k}")
+    f = getattr(lib, f"{mb.symbol}_abi")
+    f.restype = ctypes.c_char_p
+    assert json.loads(f().decode()) == json.loads(mb.abi.to_json())
+    size = getattr(lib, f"{mb.symbol}_abi_size")
+    size.restype = ctypes.c_longlong
+    fields = [(x.name, {"i64": ctypes.c_longlong, "f64": ctypes.c_double}.get(x.ctype, ctypes.c_void_p))
+              for x in mb.abi.fields]
+    assert size() == ctypes.sizeof(type("S", (ctypes.Structure,), {"_fields_": fields}))
+
+
+def test_runner_fails_loudly_without_device():
+    from paper_1905_02241_b200 import runtime as rt
+
+    if rt.device_count() > 0:
+        pytest.skip("a device is visible")
+    from paper_1905_02241_b200.runner import CudaRunner
+
+    with pytest.raises(rt.CudaError, match="no CPU fallback"):
+        CudaRunner(load_ir("corpus_cat"))
+
+
+# ---- host logic --------------------------------------------------------------------
+
+
+def test_tile_nodes_cover_all_nodes():
+    from paper_1905_02241_b200.runner import tile_nodes_for
+
+    rng = np.random.default_rng(0)
+    for n, n_nodes, t in [(10000, 1000, 512), (100, 3, 16), (5000, 5000, 1536), (7, 1, 2)]:
+        idx = rng.integers(0, n_nodes, n)
+        offsets = np.concatenate([[0], np.cumsum(np.bincount(idx, minlength=n_nodes))])
+        tiles = tile_nodes_for(offsets, t)
+        assert tiles[0] == 0 and tiles[-1] == n_nodes
+        assert np.all(np.diff(tiles) > 0)
+        sizes = offsets[tiles[1:]] - offsets[tiles[:-1]]
+        assert sizes.sum() == n
+        maxseg = np.max(np.diff(offsets))
+        assert np.all(sizes <= t + maxseg)
+
+
+def test_product_init_matches_oracle_init():
+    """Synthetic inputs are the reference's init format (interp.py:61-84)."""
+    from oracle import interp_np as O
+    from paper_1905_02241_b200.instance import init
+
+    for stem in ("hh_subset", "ProbAMPANMDA_EMS", "cdp5ish"):
+        ir = load_ir(stem)
+        a, b = init(ir, 100, 42), O.init(ir, 100, 42)
+        assert list(a.arrays) == list(b.arrays)
+        for k in a.arrays:
+            np.testing.assert_array_equal(a.arrays[k], b.arrays[k])
+        assert a.scalars == b.scalars
+
+
+def test_node_oracle_layout_is_stable_sort():
+    from oracle.nodes_np import scatter_layout
+
+    idx = np.array([3, 1, 3, 0, 1, 3], dtype=np.int32)
+    perm, offsets, rank = scatter_layout(idx, 5)
+    assert perm.tolist() == [3, 1, 4, 0, 2, 5]
+    assert offsets.tolist() == [0, 1, 3, 3, 6, 6]
+    assert np.all(perm[rank] == np.arange(6))

@@ -1,0 +1,84 @@
+"""Kernel tuning sweep (GPU): launch-shape options per mechanism.
+
+    python tools/tune.py [stem ...]
+
+Prints one JSON line per (mechanism, options): launch time from CUDA events
+(L2 flushed between launches when the working set is L2-sized), achieved
+algorithmic GB/s and instance-steps/s.  Used to pick bench.py's options.
+"""
+
+import json
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import ctypes as C  # noqa: E402
+
+from paper_1905_02241_b200 import runtime as rt  # noqa: E402
+from paper_1905_02241_b200.codegen_cuda import CudaOptions  # noqa: E402
+from paper_1905_02241_b200.instance import init, node_layout  # noqa: E402
+from paper_1905_02241_b200.ir import MechIR  # noqa: E402
+from paper_1905_02241_b200.runner import CudaRunner  # noqa: E402
+from paper_1905_02241_b200.traffic import launch_bytes  # noqa: E402
+
+SIZES = {"hh_subset": 1_000_000, "ProbAMPANMDA_EMS": 10_000_000, "na6": 1_000_000, "cdp5ish": 1_000_000,
+         "NaTs2_t": 3_333_333, "K_Pst": 3_333_333, "Ca_HVA": 3_333_333}
+VARIANTS = [
+    CudaOptions(ilp=1), CudaOptions(ilp=2), CudaOptions(ilp=1, min_blocks=4), CudaOptions(ilp=1, min_blocks=3),
+    CudaOptions(ilp=1, block=128), CudaOptions(ilp=2, min_blocks=3), CudaOptions(ilp=1, block=128, min_blocks=8),
+]
+
+
+def run(stem, opts, nodes=0, steps=30):
+    ir = MechIR.load(ROOT / "fixtures" / "ir" / f"{stem}.json")
+    n = SIZES.get(stem, 1_000_000)
+    r = CudaRunner(ir, options=opts)
+    dev = r.to_device(init(ir, n, 42))
+    kernel = "step"
+    if nodes:
+        idx, nv = node_layout(n, nodes, 42)
+        r.bind_nodes(dev, idx, nv)
+        kernel = "step_nodes"
+    r.run_kernel(dev, "initialize", 1)
+    info = rt.device_info(0)
+    lb = launch_bytes(r.abi, n, kernel, nodes)
+    flush = rt.DeviceBuffer(2 * info["l2_bytes"]) if lb < 3 * info["l2_bytes"] else None
+    a, b = rt.Event(), rt.Event()
+    for _ in range(10):
+        r.launch(dev, kernel, 1)
+    r.stream.sync()
+    total = 0.0
+    for _ in range(steps):
+        if flush:
+            rt.check(rt.lib().nmodl_l2_flush(C.c_void_p(flush.ptr), flush.nbytes // 8, C.c_void_p(r.stream.handle)), "f")
+        a.record(r.stream)
+        r.launch(dev, kernel, 1)
+        b.record(r.stream)
+        b.sync()
+        total += a.elapsed_ms(b)
+    r.check(dev)
+    ms = total / steps
+    return {"stem": stem, "opts": opts.__dict__ if hasattr(opts, "__dict__") else str(opts), "kernel": kernel, "n": n,
+            "ms": ms, "GBps": lb / (ms / 1e3) / 1e9, "inst_steps_per_s": n / (ms / 1e3), "flush": bool(flush)}
+
+
+def main():
+    stems = sys.argv[1:] or ["hh_subset", "NaTs2_t", "na6", "cdp5ish", "ProbAMPANMDA_EMS"]
+    rt.require_device(0)
+    for stem in stems:
+        for opts in VARIANTS:
+            nodes = 1_000_000 if stem == "ProbAMPANMDA_EMS" else 0
+            if nodes and opts.ilp == 2:
+                continue
+            try:
+                res = run(stem, opts, nodes)
+            except Exception as exc:  # noqa: BLE001
+                res = {"stem": stem, "opts": str(opts), "error": repr(exc)[:300]}
+            print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -65,22 +65,29 @@ WORKLOADS = {
 DEFAULT_WORKLOAD = "synapse10m"
 
 
-def bench_options():
+def options_for(stem: str):
+    """Launch shapes picked with tools/tune.py on B200 (profiles/tune_r01.md)."""
     from paper_1905_02241_b200.codegen_cuda import CudaOptions
 
-    return {"direct": CudaOptions(ilp=2), "nodes": CudaOptions()}
+    tuned = {
+        "hh_subset": CudaOptions(ilp=1, min_blocks=4),
+        "cdp5ish": CudaOptions(ilp=1, min_blocks=3),
+        "NaTs2_t": CudaOptions(ilp=2, min_blocks=3),
+        "K_Pst": CudaOptions(ilp=2, min_blocks=3),
+        "Ca_HVA": CudaOptions(ilp=2, min_blocks=3),
+    }
+    return tuned.get(stem, CudaOptions())
 
 
 def bench_irs():
     """(IR, options) pairs bench.py launches -- prebuilt by __graft_entry__.build()."""
     from paper_1905_02241_b200.ir import MechIR
 
-    opts = bench_options()
     out = []
     for w in WORKLOADS.values():
         for stem, _ in w["mechs"]:
             ir = MechIR.load(ROOT / "fixtures" / "ir" / f"{stem}.json")
-            out.append((ir, opts["nodes"] if w["nodes"] else opts["direct"]))
+            out.append((ir, options_for(stem)))
     return out
 
 
@@ -165,7 +172,7 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
-        if self.world > 1:
+        if self.world > 1 or os.environ.get("TORCHELASTIC_RUN_ID"):
             import torch
             import torch.distributed as dist
 
@@ -257,10 +264,8 @@ def run_workload(name, args, dist, stream_timing=True):
     from paper_1905_02241_b200 import runtime as rt
 
     w = WORKLOADS[name]
-    opts = bench_options()
     seed = 42 + dist.rank
-    pops = [Population(stem, n, w["nodes"], seed, opts["nodes"] if w["nodes"] else opts["direct"])
-            for stem, n in w["mechs"]]
+    pops = [Population(stem, n, w["nodes"], seed, options_for(stem)) for stem, n in w["mechs"]]
     for p in pops:
         p.setup_device()
     info = rt.device_info(dist.local)
@@ -383,12 +388,11 @@ def e2e_measure(name, dist, calls=2, timesteps=1000):
     from paper_1905_02241_b200.runner import CudaRunner, simulate, simulate_nodes
 
     w = WORKLOADS[name]
-    opts = bench_options()
     seed = 42 + dist.rank
     jobs = []
     for stem, n in w["mechs"]:
         ir = MechIR.load(ROOT / "fixtures" / "ir" / f"{stem}.json")
-        runner = CudaRunner(ir, options=opts["nodes"] if w["nodes"] else opts["direct"])
+        runner = CudaRunner(ir, options=options_for(stem))
         data = init(ir, n, seed)
         pins = [rt.PinnedRegistration(a) for a in list(data.arrays.values()) + list(data.acc.values())]
         extra = None

@@ -210,3 +210,39 @@ def test_node_oracle_layout_is_stable_sort():
     assert perm.tolist() == [3, 1, 4, 0, 2, 5]
     assert offsets.tolist() == [0, 1, 3, 3, 6, 6]
     assert np.all(perm[rank] == np.arange(6))
+
+
+def test_constant_division_is_correctly_rounded():
+    """nmodl::div_c's Markstein sequence equals IEEE a/c (checked with exact
+    rational arithmetic, including near-power-of-two adversarial numerators),
+    for the divisor literals that appear in the fixtures."""
+    import math
+    import random
+    from fractions import Fraction as Fr
+
+    from paper_1905_02241_b200.ir import iter_nodes
+
+    rn = lambda x: float(x)
+    fma = lambda a, b, c: rn(Fr(a) * Fr(b) + Fr(c))
+    consts = set()
+    for stem in all_ir_stems():
+        ir = load_ir(stem)
+        for stmts in list(ir.kernels.values()) + [(f,) for f in ir.functions.values()]:
+            for s in stmts:
+                for n in iter_nodes(s):
+                    if n.kind == "Binary" and n.attrs["op"] == "/" and n.children[1].kind == "Number":
+                        c = n.children[1].attrs["value"]
+                        if c != 0 and abs(math.frexp(c)[0]) != 0.5:
+                            consts.add(c)
+    assert consts
+    rng = random.Random(3)
+    for c in sorted(consts):
+        y = rn(Fr(1) / Fr(c))
+        for _ in range(300):
+            e = rng.randint(-900, 900)
+            a = math.ldexp(rng.random() + 1.0, e) * rng.choice((1, -1))
+            if rng.random() < 0.3:
+                a = math.nextafter(math.ldexp(1.0, e), math.inf if rng.random() < 0.5 else 0.0)
+            q = rn(Fr(a) * Fr(y))
+            q1 = fma(fma(-c, q, a), y, q)
+            assert q1 == rn(Fr(a) / Fr(c)), (c, a)

@@ -111,6 +111,8 @@ int nmodl_permute(const double *src, double *dst, const long long *perm, long lo
                   nmodl_stream_t s);
 int nmodl_permute_i32(const int *src, int *dst, const long long *perm, long long n, nmodl_stream_t s);
 int nmodl_gather_v(const double *node_v, const int *node_index, double *v, long long n, nmodl_stream_t s);
+/* self-test: out_a[i] = nmodl::exp_c(x[i]), out_b[i] = exp(x[i]) (bit-equality check) */
+int nmodl_selftest_exp(const double *x, double *out_a, double *out_b, long long n, nmodl_stream_t s);
 
 /* ---- per-mechanism library (lib<mech>-<hash>.so) -----------------------
  * Every generated mechanism exports exactly these symbols.  `md` points to a

@@ -10,6 +10,7 @@
 // scatter layout (stable counting sort by node).
 #include <cuda_runtime.h>
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
@@ -285,29 +286,12 @@ __global__ void k_hist(const int* __restrict__ node_index, long long n, int n_no
   }
 }
 
-// single-block exclusive scan over counts -> offsets (N+1 entries), chunked
-__global__ void k_scan(const unsigned int* counts, int n_nodes, long long* offsets) {
-  __shared__ long long s_carry;
-  __shared__ long long s_buf[1024];
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
-  for (int base = 0; base < n_nodes; base += 1024) {
-    int i = base + threadIdx.x;
-    long long v = (i < n_nodes) ? (long long)counts[i] : 0;
-    s_buf[threadIdx.x] = v;
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {
-      long long t = (threadIdx.x >= off) ? s_buf[threadIdx.x - off] : 0;
-      __syncthreads();
-      s_buf[threadIdx.x] += t;
-      __syncthreads();
-    }
-    if (i < n_nodes) offsets[i] = s_carry + s_buf[threadIdx.x] - v;
-    __syncthreads();
-    if (threadIdx.x == 1023) s_carry += s_buf[1023];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) offsets[n_nodes] = s_carry;
+// counts (u32) -> int64 with a trailing zero so an exclusive scan over n+1
+// entries yields offsets[n_nodes] = total
+__global__ void k_widen(const unsigned int* counts, int n_nodes, long long* out) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i <= n_nodes;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = i < n_nodes ? (long long)counts[i] : 0;
 }
 
 // Stable placement: CUB's LSD radix sort of (node, instance) pairs is stable,
@@ -338,7 +322,16 @@ NMODL_API int nmodl_scatter_layout(const int* node_index_dev, long long n, int n
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
   k_hist<<<blocks, 256, 0, s>>>(node_index_dev, n, n_nodes, counts_dev, bad_dev);
-  k_scan<<<1, 1024, 0, s>>>(counts_dev, n_nodes, offsets_dev);
+  // offsets[0..n_nodes] = exclusive scan of counts (int64), via CUB
+  k_widen<<<blocks, 256, 0, s>>>(counts_dev, n_nodes, offsets_dev);
+  {
+    size_t scan_bytes = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, offsets_dev, offsets_dev, (int64_t)n_nodes + 1, s));
+    void* scan_tmp = nullptr;
+    CK(cudaMallocAsync(&scan_tmp, scan_bytes ? scan_bytes : 16, s));
+    CK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, offsets_dev, offsets_dev, (int64_t)n_nodes + 1, s));
+    CK(cudaFreeAsync(scan_tmp, s));
+  }
   k_iota_rank<<<blocks, 256, 0, s>>>(scratch_dev, n);
   int* keys_out = nullptr;
   CK(cudaMallocAsync((void**)&keys_out, sizeof(int) * (size_t)(n > 0 ? n : 1), s));
@@ -411,6 +404,22 @@ NMODL_API int nmodl_gather_v(const double* node_v, const int* node_index, double
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
   k_gather_v<<<blocks, 256, 0, s>>>(node_v, node_index, v, n);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// self-test: nmodl::exp_c against CUDA exp() on the same inputs
+#include "nmodl_b200/mechanism.cuh"
+__global__ void k_selftest_exp(const double* __restrict__ x, double* __restrict__ a, double* __restrict__ b,
+                               long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    a[i] = nmodl::exp_c(x[i]);
+    b[i] = exp(x[i]);
+  }
+}
+NMODL_API int nmodl_selftest_exp(const double* x, double* a, double* b, long long n, cudaStream_t s) {
+  k_selftest_exp<<<256, 256, 0, s>>>(x, a, b, n);
   CK(cudaGetLastError());
   return 0;
 }

@@ -402,14 +402,20 @@ def e2e_measure(name, dist, calls=2, timesteps=1000):
             pins += [rt.PinnedRegistration(idx), rt.PinnedRegistration(nv)]
         jobs.append((ir, runner, data, extra, pins, n))
 
+    phases = {}
+
     def one_call():
         for ir, runner, data, extra, _, n in jobs:
             if extra is None:
                 simulate(ir, data, timesteps, runner=runner)
             else:
-                simulate_nodes(ir, data, timesteps, extra[0], extra[1], runner=runner)
+                t = {}
+                simulate_nodes(ir, data, timesteps, extra[0], extra[1], runner=runner, timings=t)
+                for k, v in t.items():
+                    phases[k] = phases.get(k, 0.0) + v
 
     one_call()  # warm-up (also primes graph/occupancy caches)
+    phases.clear()
     dist.barrier()
     t0 = time.perf_counter()
     for _ in range(calls):
@@ -426,6 +432,7 @@ def e2e_measure(name, dist, calls=2, timesteps=1000):
                 + (", node_index upload + device sort, node rhs/d download" if w["nodes"] else ""),
         "timesteps_per_call": timesteps,
         "calls": calls,
+        "phase_seconds_per_call": {k: v / calls for k, v in phases.items()},
     }
 
 

@@ -520,7 +520,7 @@ def simulate(layout, data, steps: int, jac_mode: str = "exact", on_step=None, ru
 
 
 def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, node_d=None,
-                   jac_mode: str = "exact", runner: CudaRunner | None = None):
+                   jac_mode: str = "exact", runner: CudaRunner | None = None, timings: dict | None = None):
     """node_index run of one mechanism population (builder extension).
 
     Per timestep: v_i = node_v[node_index[i]]; nrn_state; nrn_cur; then
@@ -528,17 +528,34 @@ def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, 
     instances i of node k in ascending instance order (deterministic; the
     oracle restatement is oracle/nodes_np.py).  Instances are initialised
     with the gathered voltage.  Returns (data, node_rhs, node_d); `data` is
-    updated in place in instance order.
+    updated in place in instance order.  `timings` (optional dict) receives
+    wall-clock seconds per phase.
     """
+    import time
+
+    clock = time.perf_counter
+    t = {}
+    t0 = clock()
     runner = runner or CudaRunner(layout, jac_mode=jac_mode)
     dev = runner.to_device(data)
+    t["upload"] = clock() - t0
+    t0 = clock()
     nb = runner.bind_nodes(dev, node_index, node_v, node_rhs, node_d)
     rt.check(rt.lib().nmodl_gather_v(C.c_void_p(nb.node_v), C.c_void_p(nb.node_index), C.c_void_p(dev.ptr["v"]),
                                      dev.n, C.c_void_p(runner.stream.handle)), "gather_v")
+    t["bind_nodes"] = clock() - t0
     try:
+        t0 = clock()
         runner.run_kernel(dev, "initialize", 1)
+        t["initialize"] = clock() - t0
+        t0 = clock()
         runner.run_kernel(dev, "step_nodes", steps)
+        t["steps"] = clock() - t0
     finally:
+        t0 = clock()
         runner.to_host(dev, data)
-    out = runner.node_arrays(dev)
+        out = runner.node_arrays(dev)
+        t["download"] = clock() - t0
+    if timings is not None:
+        timings.update(t)
     return data, out["node_rhs"], out["node_d"]

@@ -27,7 +27,7 @@ from paper_1905_02241_b200.traffic import launch_bytes  # noqa: E402
 SIZES = {"hh_subset": 1_000_000, "ProbAMPANMDA_EMS": 10_000_000, "na6": 1_000_000, "cdp5ish": 1_000_000,
          "NaTs2_t": 3_333_333, "K_Pst": 3_333_333, "Ca_HVA": 3_333_333}
 SHAPES = [dict(ilp=1), dict(ilp=2), dict(ilp=1, min_blocks=4), dict(ilp=1, min_blocks=3), dict(ilp=2, min_blocks=3)]
-CODEGEN = [dict(exp_c=False, const_pool=False), dict(), dict(fast_div=True)]
+CODEGEN = [dict(fast_path=False), dict()]
 VARIANTS = [CudaOptions(**a, **b) for b in CODEGEN for a in SHAPES]
 
 

@@ -70,11 +70,13 @@ def options_for(stem: str):
     from paper_1905_02241_b200.codegen_cuda import CudaOptions
 
     tuned = {
-        "hh_subset": CudaOptions(ilp=1, min_blocks=4),
-        "cdp5ish": CudaOptions(ilp=1, min_blocks=3),
-        "NaTs2_t": CudaOptions(ilp=2, min_blocks=3),
-        "K_Pst": CudaOptions(ilp=2, min_blocks=3),
-        "Ca_HVA": CudaOptions(ilp=2, min_blocks=3),
+        "ProbAMPANMDA_EMS": CudaOptions(ilp=1, fast_path=False),
+        "hh_subset": CudaOptions(ilp=1, min_blocks=4, fast_path=False),
+        "NaTs2_t": CudaOptions(ilp=2),
+        "K_Pst": CudaOptions(ilp=2),
+        "Ca_HVA": CudaOptions(ilp=2),
+        "na6": CudaOptions(ilp=1),
+        "cdp5ish": CudaOptions(ilp=1),
     }
     return tuned.get(stem, CudaOptions())
 

@@ -65,7 +65,12 @@ def run(stem, opts, nodes=0, steps=30):
 
 
 def main():
-    stems = sys.argv[1:] or ["hh_subset", "NaTs2_t", "na6", "cdp5ish", "ProbAMPANMDA_EMS"]
+    global VARIANTS
+    args = sys.argv[1:]
+    if args and args[0] == "--quick":
+        VARIANTS = [CudaOptions(ilp=i, fast_path=f) for f in (False, True) for i in (1, 2)]
+        args = args[1:]
+    stems = args or ["hh_subset", "NaTs2_t", "na6", "cdp5ish", "ProbAMPANMDA_EMS"]
     rt.require_device(0)
     for stem in stems:
         for opts in VARIANTS:

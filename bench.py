@@ -61,6 +61,8 @@ WORKLOADS = {
         "nodes": 0,
     },
     "kinetic1m": {"config": BASELINE["configs"][3], "mechs": [("na6", 1_000_000), ("cdp5ish", 1_000_000)], "nodes": 0},
+    # configs[4]: strong scaling -- the column is fixed, cells are split over ranks
+    "column": {"config": BASELINE["configs"][4], "mechs": [], "nodes": 0, "cells": 100_000},
 }
 DEFAULT_WORKLOAD = "synapse10m"
 
@@ -342,8 +344,13 @@ def run_workload(name, args, dist, stream_timing=True):
     achieved = dom.launch_bytes() / (dom_ms / 1e3) / 1e9
     from paper_1905_02241_b200.traffic import describe
 
+    from paper_1905_02241_b200.parallel import device_checksums, gather_checksums
+
+    local = np.concatenate([device_checksums(p.runner, p.dev) for p in pops])
+    table = gather_checksums(local, device=f"cuda:{dist.local}" if dist.pg else None)
     res = {
         "value": value,
+        "checksum_of_checksums": float(np.sum(table[..., 1])),
         "ms_per_step": max_ms / K,
         "n_rank": n_rank,
         "clocks": clocks,
@@ -372,6 +379,55 @@ def run_workload(name, args, dist, stream_timing=True):
         "pops": pops,
     }
     return res
+
+
+def run_column(args, dist):
+    """configs[4]: 100k-cell synthetic column, cells partitioned over ranks by
+    per-cell bytes/step (parallel.partition_cells); strong scaling."""
+    from paper_1905_02241_b200 import runtime as rt
+    from paper_1905_02241_b200.column import ColumnShard, ColumnSpec
+    from paper_1905_02241_b200.parallel import gather_checksums, partition_cells
+
+    spec = ColumnSpec(n_cells=WORKLOADS["column"]["cells"])
+    bounds = partition_cells(np.full(spec.n_cells, spec.cell_cost()), dist.world)
+    shard = ColumnShard(spec, int(bounds[dist.rank]), int(bounds[dist.rank + 1]), options_for)
+    s0 = shard.stream
+    K, W = args.steps, args.warmup
+    shard.launch(W)
+    s0.sync()
+    shard.check()
+    ev_a, ev_b = rt.Event(), rt.Event()
+    graph = rt.capture(s0, lambda: shard.launch(K))
+    dist.barrier()
+    visible = os.environ.get("CUDA_VISIBLE_DEVICES")
+    phys = int(visible.split(",")[dist.local]) if visible and visible.split(",")[0].isdigit() else dist.local
+    with ClockSampler(phys) as clk:
+        ev_a.record(s0)
+        graph.launch(s0)
+        ev_b.record(s0)
+        ev_b.sync()
+    ms = ev_a.elapsed_ms(ev_b)
+    shard.check()
+    dist.barrier()
+    max_ms = dist.allreduce([ms], "max")[0]
+    n_all = dist.allreduce([float(shard.n_instances)], "sum")[0]
+    table = gather_checksums(shard.checksums(), device=f"cuda:{dist.local}" if dist.pg else None)
+    peak, peak_src = _peaks()
+    achieved = shard.launch_bytes() / (ms / K / 1e3) / 1e9
+    return {
+        "value": n_all * K / (max_ms / 1e3),
+        "ms_per_step": max_ms / K,
+        "n_rank": shard.n_instances,
+        "clocks": clk.summary(),
+        "gpu_launches": K * 7,
+        "l2": "inputs larger than L2 (no flush)",
+        "roofline": {"bound": "hbm", "kernel": "7 x <mech>_k_step_nodes (whole step)", "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "bytes_per_launch": shard.launch_bytes()},
+        "checksum_of_checksums": float(np.sum(table[..., 1])),
+        "cells_per_rank": [int(b) for b in np.diff(bounds)],
+        "per_mechanism": {m: {"instances": shard.devs[m].n} for m in shard.devs},
+    }
 
 
 def C_void(x):
@@ -423,6 +479,7 @@ def e2e_measure(name, dist, calls=2, timesteps=1000):
     for _ in range(calls):
         one_call()
     dt = time.perf_counter() - t0
+    phases["unaccounted"] = dt - sum(phases.values())
     dt = dist.allreduce([dt], "max")[0]
     n_all = dist.allreduce([float(sum(j[5] for j in jobs))], "sum")[0]
     return {
@@ -555,10 +612,17 @@ def main():
     from paper_1905_02241_b200 import runtime as rt
 
     rt.require_device(dist.local)
-    res = run_workload(args.workload, args, dist)
-    e2e = None if args.no_e2e else e2e_measure(args.workload, dist)
+    if args.workload == "column":
+        res = run_column(args, dist)
+        e2e = None
+        config["cells"] = WORKLOADS["column"]["cells"]
+        config["instances_per_gpu"] = None
+        config["parallelism"] = f"{args.gpus} x cell shard (strong scaling, no per-step collective; NCCL checksum gather)"
+    else:
+        res = run_workload(args.workload, args, dist)
+        e2e = None if args.no_e2e else e2e_measure(args.workload, dist)
     also = {}
-    if not args.no_also:
+    if not args.no_also and args.workload != "column":
         for other in ("hh1m", "bbp20m", "kinetic1m"):
             if other == args.workload:
                 continue
@@ -569,7 +633,7 @@ def main():
                            "per_mechanism": r["per_mechanism"]}
             del r
     cpu = None
-    if dist.rank == 0 and args.gpus == 1:
+    if dist.rank == 0 and args.gpus == 1 and args.workload != "column":
         cpu = cpu_reference(args.workload)
     if dist.rank == 0:
         config["l2_policy"] = res["l2"]
@@ -582,7 +646,7 @@ def main():
             "warmup": args.warmup,
             "ms_per_step": res["ms_per_step"],
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if args.workload == "column" else "weak",
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (modlc.interp.init-format seeded instance store; random node_index)",
@@ -593,6 +657,8 @@ def main():
             "gpu_launches": res["gpu_launches"],
             "clocks": res["clocks"],
             "per_mechanism": res["per_mechanism"],
+            "validation": {"checksum_of_checksums": res.get("checksum_of_checksums"),
+                           "how": "per-array sum|x| on each GPU (fixed-tree device reduction), all-gathered with NCCL"},
             "also": also,
         }
         print(json.dumps(line), flush=True)

@@ -1,0 +1,161 @@
+"""Synthetic cortical column (BASELINE configs[4]): every mechanism of a cell
+population stepped together, sharded by cell.
+
+Builder-defined workload (the reference has no cells, nodes or ion sharing;
+SPEC.md:441, modlc/layout.py:124-128).  Cell c owns compartments (nodes)
+[c*(1+D), (c+1)*(1+D)); node 0 of a cell is the soma.
+
+  soma, one instance per cell:  NaTs2_t, K_Pst, Ca_HVA, CaDynamics_E2, SKv3_1
+  soma + every dendrite:        Ih
+  S synapses per cell:          ProbAMPANMDA_EMS on random compartments of the cell
+
+Per timestep the populations run in LAUNCH_ORDER, each one fused kernel that
+gathers v from the shared node voltage, runs nrn_state + nrn_cur and folds its
+currents into the shared node rhs/d in instance order.  CaDynamics_E2 reads
+Ca_HVA's `ica` array directly (ion coupling; Ca_HVA is launched first), which
+is what NEURON's shared ion arrays do.  Instance data are drawn with
+`init_range`, so a shard of cells [lo, hi) holds exactly the instances the
+single-GPU column holds for those cells: shard checksums add up across ranks.
+"""
+
+from __future__ import annotations
+
+import zlib
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+from .instance import V_RANGE, init_range
+from .ir import MechIR
+
+FIXTURES = Path(__file__).resolve().parent.parent / "fixtures" / "ir"
+SOMA_MECHS = ("NaTs2_t", "K_Pst", "Ca_HVA", "cadyn", "SKv3_1")
+LAUNCH_ORDER = ("NaTs2_t", "K_Pst", "Ca_HVA", "cadyn", "SKv3_1", "Ih", "ProbAMPANMDA_EMS")
+COUPLINGS = (("cadyn", "ica", "Ca_HVA", "ica"),)  # consumer slot <- producer slot
+
+
+@dataclass(frozen=True)
+class ColumnSpec:
+    n_cells: int = 100_000
+    dend_per_cell: int = 20
+    syn_per_cell: int = 100
+    seed: int = 42
+
+    @property
+    def nodes_per_cell(self) -> int:
+        return 1 + self.dend_per_cell
+
+    def instances_per_cell(self, stem: str) -> int:
+        if stem in SOMA_MECHS:
+            return 1
+        if stem == "Ih":
+            return self.nodes_per_cell
+        if stem == "ProbAMPANMDA_EMS":
+            return self.syn_per_cell
+        raise KeyError(stem)
+
+    def cell_cost(self) -> float:
+        """Bytes one cell moves per timestep (for cost-balanced sharding)."""
+        per_inst = {"ProbAMPANMDA_EMS": 171.0, "Ih": 56.0, "SKv3_1": 64.0, "cadyn": 72.0}
+        return sum(self.instances_per_cell(m) * per_inst.get(m, 80.0) for m in LAUNCH_ORDER)
+
+
+def shard_layout(spec: ColumnSpec, cell_lo: int, cell_hi: int) -> dict:
+    """Per mechanism: (global instance range, node_index local to the shard);
+    plus the shard's node voltages."""
+    npc = spec.nodes_per_cell
+    ncell = cell_hi - cell_lo
+    cells = np.arange(cell_lo, cell_hi, dtype=np.int64)
+    out = {}
+    for stem in LAUNCH_ORDER:
+        k = spec.instances_per_cell(stem)
+        lo, hi = cell_lo * k, cell_hi * k
+        local_cell = np.repeat(np.arange(ncell, dtype=np.int64), k)
+        if stem in SOMA_MECHS:
+            comp = np.zeros(ncell * k, dtype=np.int64)
+        elif stem == "Ih":
+            comp = np.tile(np.arange(npc, dtype=np.int64), ncell)
+        else:  # synapses: compartment drawn per global synapse id (shard-independent)
+            bg = np.random.PCG64(np.random.SeedSequence([spec.seed, zlib.crc32(b"syn_comp")]))
+            bg.advance(lo)
+            u = np.random.Generator(bg).random(hi - lo)  # one 64-bit draw per synapse
+            comp = np.minimum((u * npc).astype(np.int64), npc - 1)
+        out[stem] = (lo, hi, (local_cell * npc + comp).astype(np.int32))
+    bg = np.random.PCG64(np.random.SeedSequence([spec.seed, zlib.crc32(b"node_v")]))
+    bg.advance(cell_lo * npc)
+    node_v = np.random.Generator(bg).uniform(*V_RANGE, ncell * npc)
+    return {"mechs": out, "node_v": node_v, "n_nodes": ncell * npc}
+
+
+def load_irs() -> dict:
+    return {stem: MechIR.load(FIXTURES / f"{stem}.json") for stem in LAUNCH_ORDER}
+
+
+class ColumnShard:
+    """All populations of cells [cell_lo, cell_hi) resident on one GPU."""
+
+    def __init__(self, spec: ColumnSpec, cell_lo: int, cell_hi: int, options_for=None):
+        from .runner import CudaRunner, NodeArrays
+
+        self.spec = spec
+        self.cells = (cell_lo, cell_hi)
+        lay = shard_layout(spec, cell_lo, cell_hi)
+        self.layout = lay
+        irs = load_irs()
+        self.runners, self.devs, self.node_index = {}, {}, {}
+        first = None
+        for stem in LAUNCH_ORDER:
+            opts = options_for(stem) if options_for else None
+            r = CudaRunner(irs[stem], options=opts)
+            if first is None:
+                first = r
+            else:
+                r.stream = first.stream  # one stream: launch order == step order
+            self.runners[stem] = r
+        self.stream = first.stream
+        self.nodes = NodeArrays(lay["node_v"], stream=self.stream)
+        for stem in LAUNCH_ORDER:
+            lo, hi, idx = lay["mechs"][stem]
+            r = self.runners[stem]
+            data = init_range(irs[stem], lo, hi, spec.seed)
+            dev = r.to_device(data)
+            r.bind_nodes(dev, idx, shared=self.nodes)
+            r.gather_voltage(dev)
+            self.devs[stem] = dev
+            self.node_index[stem] = idx
+        for dst, dslot, src, sslot in COUPLINGS:
+            self.runners[dst].share_slot(self.devs[dst], dslot, self.devs[src], sslot)
+        for stem in LAUNCH_ORDER:
+            self.runners[stem].run_kernel(self.devs[stem], "initialize", 1)
+
+    @property
+    def n_instances(self) -> int:
+        return sum(d.n for d in self.devs.values())
+
+    def launch(self, steps: int = 1) -> None:
+        for _ in range(steps):
+            for stem in LAUNCH_ORDER:
+                self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
+
+    def check(self) -> None:
+        for stem in LAUNCH_ORDER:
+            self.runners[stem].check(self.devs[stem])
+
+    def launch_bytes(self) -> int:
+        from .traffic import launch_bytes
+
+        total = 0
+        for stem in LAUNCH_ORDER:
+            d = self.devs[stem]
+            total += launch_bytes(self.runners[stem].abi, d.n, "step_nodes", 0)
+        return total + 32 * self.nodes.n_nodes * len(LAUNCH_ORDER)
+
+    def checksums(self) -> np.ndarray:
+        from .parallel import device_checksums
+
+        rows = []
+        for stem in LAUNCH_ORDER:
+            r, d = self.runners[stem], self.devs[stem]
+            rows.append(device_checksums(r, d, [s for s in r.abi.slots if s in d.ptr] + ["i_acc", "g_acc"]))
+        return np.concatenate(rows)

@@ -57,6 +57,44 @@ def init(layout, n: int, seed: int, dt: float = 0.025) -> HostInstanceData:
     return HostInstanceData(n, arrays, {"i_acc": np.zeros(n), "g_acc": np.zeros(n)}, scalars)
 
 
+def _range_rng(seed: int, name: str, lo: int) -> np.random.Generator:
+    """The `_slot_rng` stream advanced to draw `lo` (one 64-bit draw per double)."""
+    bg = np.random.PCG64(np.random.SeedSequence([seed, zlib.crc32(name.encode())]))
+    bg.advance(lo)
+    return np.random.Generator(bg)
+
+
+def init_range(layout, lo: int, hi: int, seed: int, dt: float = 0.025) -> HostInstanceData:
+    """Instances [lo, hi) of `init(layout, N, seed)` for any N >= hi, without
+    materialising the prefix -- so each rank of a sharded run draws exactly
+    the instances it owns and the union over ranks is the single-GPU store."""
+    ir = from_layout(layout)
+    n = hi - lo
+    if n < 1:
+        raise ValueError("need at least one instance")
+    arrays = {}
+    for slot in ir.slots:
+        if slot.role == "parameter":
+            arrays[slot.name] = np.full(n, slot.default if slot.default is not None else 0.0)
+            continue
+        if slot.ion_kind == "current":
+            arrays[slot.name] = np.zeros(n)
+            continue
+        rng = _range_rng(seed, slot.name, lo)
+        if slot.ion_kind == "conc":
+            arrays[slot.name] = rng.uniform(*CONC_RANGE, n)
+        elif slot.ion_kind == "reversal":
+            arrays[slot.name] = rng.uniform(*REVERSAL_RANGE, n)
+        elif slot.role == "state":
+            arrays[slot.name] = rng.uniform(*STATE_RANGE, n)
+        else:
+            arrays[slot.name] = rng.uniform(*ASSIGNED_RANGE, n)
+    arrays["v"] = _range_rng(seed, "v", lo).uniform(*V_RANGE, n)
+    scalars = dict(ir.global_scalars)
+    scalars["dt"] = dt
+    return HostInstanceData(n, arrays, {"i_acc": np.zeros(n), "g_acc": np.zeros(n)}, scalars)
+
+
 def node_layout(n: int, n_nodes: int, seed: int):
     """(node_index int32[n], node_v float64[n_nodes]) for the scatter workload."""
     rng = np.random.default_rng([seed, zlib.crc32(b"node_index")])

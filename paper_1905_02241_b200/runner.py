@@ -95,6 +95,51 @@ class NodeBinding:
         self.buffers.append(b)
         return b.ptr
 
+    def host_array(self, name: str, stream) -> np.ndarray:
+        """Host copy of the int64 perm/rank arrays, fetched on first use
+        (error remapping, tests) -- never on the stepping path."""
+        cache = self.__dict__.setdefault("_host", {})
+        if name not in cache:
+            arr = np.empty(self.n, dtype=np.int64)
+            rt.d2h(arr.ctypes.data, getattr(self, name), arr.nbytes, stream)
+            stream.sync()
+            cache[name] = arr
+        return cache[name]
+
+    @property
+    def perm_host(self):
+        return self.host_array("perm", self.stream)
+
+
+class NodeArrays:
+    """Device node arrays (voltage, rhs, d) shared by several mechanism
+    populations of one cell set (a compartment is one node)."""
+
+    def __init__(self, node_v, node_rhs=None, node_d=None, stream=None):
+        node_v = np.ascontiguousarray(node_v, dtype=np.float64)
+        self.n_nodes = int(node_v.shape[0])
+        nb = self.n_nodes * 8
+        self.buffers = [rt.DeviceBuffer(nb) for _ in range(3)]
+        self.node_v, self.node_rhs, self.node_d = (b.ptr for b in self.buffers)
+        s = stream or rt.Stream()
+        rt.h2d(self.node_v, node_v.ctypes.data, nb, s)
+        for ptr, host in ((self.node_rhs, node_rhs), (self.node_d, node_d)):
+            if host is None:
+                rt.memset(ptr, 0, nb, s)
+            else:
+                h = np.ascontiguousarray(host, dtype=np.float64)
+                rt.h2d(ptr, h.ctypes.data, nb, s)
+        s.sync()
+
+    def download(self, stream) -> dict:
+        out = {}
+        for name in ("node_v", "node_rhs", "node_d"):
+            arr = np.empty(self.n_nodes)
+            rt.d2h(arr.ctypes.data, getattr(self, name), arr.nbytes, stream)
+            out[name] = arr
+        stream.sync()
+        return out
+
 
 class DeviceInstanceData:
     """Device-resident SoA store: one arena, 256-byte aligned arrays."""
@@ -375,18 +420,27 @@ class CudaRunner:
             raise _interp_error(self._message(st.err_key, st, dev))
 
     # ---- node_index extension ----------------------------------------------------------
-    def bind_nodes(self, dev: DeviceInstanceData, node_index, node_v, node_rhs=None, node_d=None,
-                   tile: int | None = None) -> NodeBinding:
-        """Attach node arrays and reorder the store node-stably on the device."""
+    def bind_nodes(self, dev: DeviceInstanceData, node_index, node_v=None, node_rhs=None, node_d=None,
+                   tile: int | None = None, shared: "NodeArrays | None" = None) -> NodeBinding:
+        """Attach node arrays and reorder the store node-stably on the device.
+
+        With `shared`, the node voltage/rhs/d arrays are the given device
+        arrays (all mechanisms of a cell population fold into the same nodes,
+        in launch order); otherwise they are allocated from the host arrays."""
         if dev.nodes is not None:
             raise ValueError("nodes already bound")
         node_index = np.ascontiguousarray(node_index, dtype=np.int32)
-        node_v = np.ascontiguousarray(node_v, dtype=np.float64)
-        n, n_nodes = dev.n, int(node_v.shape[0])
+        if shared is None:
+            node_v = np.ascontiguousarray(node_v, dtype=np.float64)
+            n_nodes = int(node_v.shape[0])
+        else:
+            n_nodes = shared.n_nodes
+        n = dev.n
         if node_index.shape != (n,):
             raise ValueError("node_index must have one entry per instance")
         nb = NodeBinding(n, n_nodes)
         s = self.stream
+        nb.stream = s
         L = rt.lib()
         idx_in = nb.alloc(4 * n)
         rt.h2d(idx_in, node_index.ctypes.data, 4 * n, s)
@@ -408,21 +462,23 @@ class CudaRunner:
         nb.node_index = nb.alloc(4 * n)
         rt.check(L.nmodl_permute_i32(C.c_void_p(idx_in), C.c_void_p(nb.node_index), C.c_void_p(nb.perm), n,
                                      C.c_void_p(s.handle)), "permute_i32")
-        nb.node_v = nb.alloc(8 * n_nodes)
-        rt.h2d(nb.node_v, node_v.ctypes.data, 8 * n_nodes, s)
-        nb.node_rhs = nb.alloc(8 * n_nodes)
-        nb.node_d = nb.alloc(8 * n_nodes)
-        for ptr, host in ((nb.node_rhs, node_rhs), (nb.node_d, node_d)):
-            if host is None:
-                rt.memset(ptr, 0, 8 * n_nodes, s)
-            else:
-                h = np.ascontiguousarray(host, dtype=np.float64)
-                rt.h2d(ptr, h.ctypes.data, 8 * n_nodes, s)
+        if shared is not None:
+            nb.node_v, nb.node_rhs, nb.node_d = shared.node_v, shared.node_rhs, shared.node_d
+            nb.shared = shared
+        else:
+            nb.node_v = nb.alloc(8 * n_nodes)
+            rt.h2d(nb.node_v, node_v.ctypes.data, 8 * n_nodes, s)
+            nb.node_rhs = nb.alloc(8 * n_nodes)
+            nb.node_d = nb.alloc(8 * n_nodes)
+            for ptr, host in ((nb.node_rhs, node_rhs), (nb.node_d, node_d)):
+                if host is None:
+                    rt.memset(ptr, 0, 8 * n_nodes, s)
+                else:
+                    h = np.ascontiguousarray(host, dtype=np.float64)
+                    rt.h2d(ptr, h.ctypes.data, 8 * n_nodes, s)
         # host copies of the (integer) layout for tiling and error remapping
         offsets = np.empty(n_nodes + 1, dtype=np.int64)
         rt.d2h(offsets.ctypes.data, nb.node_offsets, offsets.nbytes, s)
-        nb.perm_host = np.empty(n, dtype=np.int64)
-        rt.d2h(nb.perm_host.ctypes.data, nb.perm, nb.perm_host.nbytes, s)
         s.sync()
         nb.offsets_host = offsets
         # target 3/4 of the shared-memory capacity so a tile rarely spills to
@@ -442,12 +498,33 @@ class CudaRunner:
         s.sync()
         dev.nodes = nb
         # prescan indices refer to instance order; remap to sorted positions
-        rank = np.empty(n, dtype=np.int64)
-        rt.d2h(rank.ctypes.data, nb.rank, rank.nbytes, s)
-        s.sync()
-        nb.rank_host = rank
-        dev.prebad = {k: int(rank[v]) for k, v in dev.prebad.items()}
+        if dev.prebad:
+            rank = nb.host_array("rank", s)
+            dev.prebad = {k: int(rank[v]) for k, v in dev.prebad.items()}
         return nb
+
+    def gather_voltage(self, dev: DeviceInstanceData) -> None:
+        """v[i] = node_v[node_index[i]] in the (node-sorted) device store."""
+        nb = dev.nodes
+        rt.check(rt.lib().nmodl_gather_v(C.c_void_p(nb.node_v), C.c_void_p(nb.node_index), C.c_void_p(dev.ptr["v"]),
+                                         dev.n, C.c_void_p(self.stream.handle)), "gather_v")
+
+    @staticmethod
+    def share_slot(dst: DeviceInstanceData, dst_slot: str, src: DeviceInstanceData, src_slot: str) -> None:
+        """Ion coupling: make `dst`'s slot the very array `src` writes (e.g.
+        Ca_HVA's ica read by CaDynamics_E2).  Both stores must hold the same
+        instances in the same order (same node_index, hence same sort); the
+        producer's launch must precede the consumer's in each timestep.  The
+        reference keeps one store per mechanism (modlc/layout.py:124-128);
+        sharing is the device-side equivalent of NEURON's ion arrays."""
+        if dst.n != src.n:
+            raise ValueError("shared ion slots need equal instance counts")
+        if (dst.nodes is None) != (src.nodes is None) or (
+            dst.nodes is not None and not np.array_equal(dst.nodes.perm_host, src.nodes.perm_host)
+        ):
+            raise ValueError("shared ion slots need identical instance order")
+        dst.ptr[dst_slot] = src.ptr[src_slot]
+        dst.shared_slots = getattr(dst, "shared_slots", set()) | {dst_slot}
 
     def node_arrays(self, dev: DeviceInstanceData) -> dict:
         nb = dev.nodes
@@ -475,12 +552,14 @@ class CudaRunner:
         # per-instance voltage is the gathered node voltage
         rt.check(L.nmodl_gather_v(C.c_void_p(nb.node_v), C.c_void_p(nb.node_index), C.c_void_p(dev.ptr["v"]),
                                   dev.n, C.c_void_p(s.handle)), "gather_v")
+        # one stream: each permute waits for the previous copy out of `tmp`,
+        # the host waits once at the end
         for name in list(dev.names) + ["i_acc", "g_acc"]:
             rt.check(L.nmodl_permute(C.c_void_p(dev.ptr[name]), C.c_void_p(tmp.ptr), C.c_void_p(nb.perm), dev.n, 1,
                                      C.c_void_p(s.handle)), "unpermute")
             dst = data.acc[name] if name in ("i_acc", "g_acc") else data.arrays[name]
             rt.d2h(dst.ctypes.data, tmp.ptr, 8 * dev.n, s)
-            s.sync()
+        s.sync()
 
 
 def tile_nodes_for(offsets: np.ndarray, tile: int) -> np.ndarray:
@@ -554,7 +633,12 @@ def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, 
     finally:
         t0 = clock()
         runner.to_host(dev, data)
-        out = runner.node_arrays(dev)
+        out = {}
+        for name in ("node_rhs", "node_d"):
+            arr = np.empty(nb.n_nodes)
+            rt.d2h(arr.ctypes.data, getattr(nb, name), arr.nbytes, runner.stream)
+            out[name] = arr
+        runner.stream.sync()
         t["download"] = clock() - t0
     if timings is not None:
         timings.update(t)

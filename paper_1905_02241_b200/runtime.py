@@ -138,17 +138,58 @@ def device_info(dev: int = 0) -> dict:
             "cc": (ma.value, mi.value), "name": name.value.decode()}
 
 
+_POOL: dict[int, list[int]] = {}
+_POOL_BYTES = 0
+_POOL_CAP = 32 << 30  # keep at most 32 GiB of freed blocks for reuse
+_pool_lock = threading.Lock()
+
+
+def empty_cache() -> None:
+    """Return every cached free block to the driver."""
+    global _POOL_BYTES
+    with _pool_lock:
+        for size, ptrs in _POOL.items():
+            for p in ptrs:
+                lib().nmodl_free(C.c_void_p(p))
+        _POOL.clear()
+        _POOL_BYTES = 0
+
+
 class DeviceBuffer:
-    """Owned device allocation."""
+    """Owned device allocation, recycled through a size-keyed cache.
+
+    cudaMalloc/cudaFree of multi-GB SoA arenas synchronise the device and
+    cost milliseconds each; a store that is uploaded, stepped and downloaded
+    repeatedly (the public `simulate` path) reuses its blocks instead."""
 
     def __init__(self, nbytes: int):
-        self.nbytes = int(nbytes)
+        global _POOL_BYTES
+        self.nbytes = int(max(nbytes, 1))
+        key = (self.nbytes + 255) // 256 * 256
+        self._key = key
+        with _pool_lock:
+            free = _POOL.get(key)
+            if free:
+                self.ptr = free.pop()
+                _POOL_BYTES -= key
+                return
         p = C.c_void_p()
-        check(lib().nmodl_malloc(C.byref(p), max(self.nbytes, 1)), f"cudaMalloc({nbytes})")
+        rc = lib().nmodl_malloc(C.byref(p), key)
+        if rc != 0:  # out of memory: drop the cache and retry once
+            empty_cache()
+            rc = lib().nmodl_malloc(C.byref(p), key)
+        check(rc, f"cudaMalloc({nbytes})")
         self.ptr = p.value
 
     def free(self) -> None:
+        global _POOL_BYTES
         if self.ptr:
+            with _pool_lock:
+                if _POOL_BYTES + self._key <= _POOL_CAP:
+                    _POOL.setdefault(self._key, []).append(self.ptr)
+                    _POOL_BYTES += self._key
+                    self.ptr = None
+                    return
             lib().nmodl_free(C.c_void_p(self.ptr))
             self.ptr = None
 

@@ -1,0 +1,54 @@
+"""Synthetic column (BASELINE configs[4]): seven populations over shared nodes,
+Ca_HVA -> CaDynamics_E2 ion coupling, vs oracle/column_np.py; and shard
+additivity (cells split across "ranks" = the single-shard checksums)."""
+
+import numpy as np
+import pytest
+
+from oracle import column_np as CN
+from oracle import interp_np as O
+from parity import TOL, parity
+
+pytestmark = pytest.mark.gpu
+
+
+def test_small_column_matches_oracle():
+    from paper_1905_02241_b200.column import COUPLINGS, LAUNCH_ORDER, ColumnShard, ColumnSpec, load_irs, shard_layout
+    from paper_1905_02241_b200.instance import init_range
+
+    spec = ColumnSpec(n_cells=300, dend_per_cell=5, syn_per_cell=12, seed=7)
+    steps = 100
+    shard = ColumnShard(spec, 0, spec.n_cells)
+    shard.launch(steps)
+    shard.check()
+    irs = load_irs()
+    lay = shard_layout(spec, 0, spec.n_cells)
+    datas = {m: init_range(irs[m], lay["mechs"][m][0], lay["mechs"][m][1], spec.seed) for m in LAUNCH_ORDER}
+    datas = {m: O.InstanceData(x.n, x.arrays, x.acc, x.scalars) for m, x in datas.items()}
+    idx = {m: lay["mechs"][m][2] for m in LAUNCH_ORDER}
+    ref, rhs, d = CN.simulate_column(irs, datas, idx, lay["node_v"], LAUNCH_ORDER, COUPLINGS, steps)
+    for m in LAUNCH_ORDER:
+        got = init_range(irs[m], lay["mechs"][m][0], lay["mechs"][m][1], spec.seed)
+        shard.runners[m].to_host(shard.devs[m], got)
+        dev, where = parity(irs[m], ref[m], got)
+        assert dev <= TOL, (m, dev, where)
+    nodes = shard.nodes.download(shard.stream)
+    for name, want in (("node_rhs", rhs), ("node_d", d)):
+        got = nodes[name]
+        den = np.maximum(np.maximum(np.abs(got), np.abs(want)), 1e-30)
+        assert np.max(np.abs(got - want) / den) <= 1e-9, name
+
+
+def test_column_shards_add_up():
+    """Two shards of cells hold exactly the single-shard instances: per-array
+    sums (checksums) of the two shards add to the whole column's."""
+    from paper_1905_02241_b200.column import ColumnShard, ColumnSpec
+
+    spec = ColumnSpec(n_cells=500, dend_per_cell=4, syn_per_cell=10, seed=3)
+    whole = ColumnShard(spec, 0, 500)
+    a, b = ColumnShard(spec, 0, 230), ColumnShard(spec, 230, 500)
+    for s in (whole, a, b):
+        s.launch(20)
+        s.check()
+    cw, ca, cb = whole.checksums(), a.checksums(), b.checksums()
+    np.testing.assert_allclose(ca[:, 1] + cb[:, 1], cw[:, 1], rtol=1e-12)

@@ -261,7 +261,8 @@ class Population:
     def launch_bytes(self):
         from paper_1905_02241_b200.traffic import launch_bytes
 
-        return launch_bytes(self.runner.abi, self.n, self.kernel, self.n_nodes)
+        touched = self.dev.nodes.n_segs if (self.dev is not None and self.dev.nodes is not None) else 0
+        return launch_bytes(self.runner.abi, self.n, self.kernel, touched)
 
 
 def run_workload(name, args, dist, stream_timing=True):

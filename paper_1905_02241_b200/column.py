@@ -148,8 +148,8 @@ class ColumnShard:
         total = 0
         for stem in LAUNCH_ORDER:
             d = self.devs[stem]
-            total += launch_bytes(self.runners[stem].abi, d.n, "step_nodes", 0)
-        return total + 32 * self.nodes.n_nodes * len(LAUNCH_ORDER)
+            total += launch_bytes(self.runners[stem].abi, d.n, "step_nodes", d.nodes.n_segs)
+        return total
 
     def checksums(self) -> np.ndarray:
         from .parallel import device_checksums

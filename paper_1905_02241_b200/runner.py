@@ -82,7 +82,8 @@ class NodeBinding:
 
     perm/rank: node-stable sort of instances (np.argsort(node_index,
     kind="stable") and its inverse); offsets: per-node instance segments in
-    sorted order; tile_nodes: CTA tiles made of whole node segments.
+    sorted order; seg_node/seg_offsets: the nodes that own instances and their
+    instance ranges; tile_segs: CTA tiles made of whole segments.
     """
 
     def __init__(self, n, n_nodes):
@@ -445,13 +446,13 @@ class CudaRunner:
         idx_in = nb.alloc(4 * n)
         rt.h2d(idx_in, node_index.ctypes.data, 4 * n, s)
         counts = nb.alloc(4 * n_nodes)
-        nb.node_offsets = nb.alloc(8 * (n_nodes + 1))
+        nb.node_offsets_full = nb.alloc(8 * (n_nodes + 1))
         scratch = nb.alloc(8 * n)
         nb.perm = nb.alloc(8 * n)
         nb.rank = nb.alloc(8 * n)
         bad = nb.alloc(4)
         rt.check(L.nmodl_scatter_layout(C.c_void_p(idx_in), n, n_nodes, C.c_void_p(counts),
-                                        C.c_void_p(nb.node_offsets), C.c_void_p(scratch), C.c_void_p(nb.perm),
+                                        C.c_void_p(nb.node_offsets_full), C.c_void_p(scratch), C.c_void_p(nb.perm),
                                         C.c_void_p(nb.rank), C.c_void_p(bad), C.c_void_p(s.handle)),
                  "scatter_layout")
         b = np.empty(1, dtype=np.int32)
@@ -478,17 +479,28 @@ class CudaRunner:
                     rt.h2d(ptr, h.ctypes.data, 8 * n_nodes, s)
         # host copies of the (integer) layout for tiling and error remapping
         offsets = np.empty(n_nodes + 1, dtype=np.int64)
-        rt.d2h(offsets.ctypes.data, nb.node_offsets, offsets.nbytes, s)
+        rt.d2h(offsets.ctypes.data, nb.node_offsets_full, offsets.nbytes, s)
         s.sync()
         nb.offsets_host = offsets
+        # segments: the nodes that own at least one instance, in node order;
+        # the reduction touches only those (sparse populations such as one
+        # channel per soma leave most compartments alone)
+        seg_node = np.flatnonzero(np.diff(offsets)).astype(np.int32)
+        seg_off = np.concatenate([offsets[seg_node], [n]]).astype(np.int64)
+        nb.n_segs = len(seg_node)
+        nb.seg_node = nb.alloc(4 * max(1, len(seg_node)))
+        nb.seg_offsets = nb.alloc(8 * len(seg_off))
+        rt.h2d(nb.seg_node, seg_node.ctypes.data, seg_node.nbytes, s)
+        rt.h2d(nb.seg_offsets, seg_off.ctypes.data, seg_off.nbytes, s)
         # target 3/4 of the shared-memory capacity so a tile rarely spills to
         # the global-memory reduction path when a segment straddles a boundary
         T = tile or max(1, (3 * self.options.tile) // 4)
-        tiles = tile_nodes_for(offsets, T)
-        nb.tile_nodes_host = tiles
-        nb.tile_nodes = nb.alloc(8 * len(tiles))
-        rt.h2d(nb.tile_nodes, tiles.ctypes.data, tiles.nbytes, s)
+        tiles = tile_nodes_for(seg_off, T)
+        nb.tile_segs_host = tiles
+        nb.tile_segs = nb.alloc(8 * len(tiles))
+        rt.h2d(nb.tile_segs, tiles.ctypes.data, tiles.nbytes, s)
         nb.n_tiles = len(tiles) - 1
+        s.sync()
         # reorder every instance array into node-sorted order (on the device)
         tmp = rt.DeviceBuffer(8 * n)
         for name in list(dev.names) + ["i_acc", "g_acc"]:
@@ -539,7 +551,7 @@ class CudaRunner:
             rt.d2h(arr.ctypes.data, ptr, arr.nbytes, self.stream)
             out[name] = arr
         offs = np.empty(nb.n_nodes + 1, dtype=np.int64)
-        rt.d2h(offs.ctypes.data, nb.node_offsets, offs.nbytes, self.stream)
+        rt.d2h(offs.ctypes.data, nb.node_offsets_full, offs.nbytes, self.stream)
         out["offsets"] = offs
         self.stream.sync()
         return out
@@ -563,7 +575,8 @@ class CudaRunner:
 
 
 def tile_nodes_for(offsets: np.ndarray, tile: int) -> np.ndarray:
-    """CTA tiles of whole node segments, ~`tile` instances each.
+    """CTA tiles of whole segments (`offsets` = segment start offsets plus the
+    total), ~`tile` instances each.
 
     Boundary nodes are the first node whose segment starts at or after each
     multiple of `tile`; a segment larger than a tile becomes its own tile

@@ -24,6 +24,7 @@ def bytes_per_instance(abi, kernel: str = "step") -> int:
 
 
 def launch_bytes(abi, n: int, kernel: str = "step", n_nodes: int = 0) -> int:
+    """`n_nodes`: nodes that own at least one instance (the ones touched)."""
     if kernel == "step_nodes":
         per = bytes_per_instance(abi, "step_nodes") + 4 + 8
         return n * per + 32 * n_nodes

@@ -171,18 +171,36 @@ class ClockSampler:
 
 
 class Dist:
+    """torchrun plumbing: one process per GPU; NCCL for the (tiny) barrier /
+    max-time / checksum collectives.  When fewer GPUs than ranks are visible
+    (a multi-rank smoke test on one GPU) ranks share devices and the
+    collectives fall back to gloo."""
+
     def __init__(self):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.device = self.local
         self.pg = None
+        self.backend = None
         if self.world > 1 or os.environ.get("TORCHELASTIC_RUN_ID"):
             import torch
             import torch.distributed as dist
 
-            torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            ndev = max(torch.cuda.device_count(), 1)
+            self.device = self.local % ndev
+            torch.cuda.set_device(self.device)
+            if ndev >= self.world:
+                self.backend = "nccl"
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.device))
+            else:
+                self.backend = "gloo"
+                dist.init_process_group("gloo")
             self.pg = dist
+
+    @property
+    def tensor_device(self):
+        return f"cuda:{self.device}" if self.backend == "nccl" else None
 
     def barrier(self):
         if self.pg:
@@ -193,7 +211,7 @@ class Dist:
             return list(values)
         import torch
 
-        t = torch.tensor(list(values), dtype=torch.float64, device=f"cuda:{self.local}")
+        t = torch.tensor(list(values), dtype=torch.float64, device=self.tensor_device or "cpu")
         self.pg.all_reduce(t, op={"max": self.pg.ReduceOp.MAX, "sum": self.pg.ReduceOp.SUM}[op])
         return t.cpu().tolist()
 
@@ -273,7 +291,7 @@ def run_workload(name, args, dist, stream_timing=True):
     pops = [Population(stem, n, w["nodes"], seed, options_for(stem)) for stem, n in w["mechs"]]
     for p in pops:
         p.setup_device()
-    info = rt.device_info(dist.local)
+    info = rt.device_info(dist.device)
     streams = [p.runner.stream for p in pops]
     working = sum(p.launch_bytes() for p in pops)
     flush = working < 3 * info["l2_bytes"]
@@ -297,7 +315,7 @@ def run_workload(name, args, dist, stream_timing=True):
     s0.sync()
     total_ms = 0.0
     visible = os.environ.get("CUDA_VISIBLE_DEVICES")
-    phys = int(visible.split(",")[dist.local]) if visible and visible.split(",")[0].isdigit() else dist.local
+    phys = int(visible.split(",")[dist.device]) if visible and visible.split(",")[0].isdigit() else dist.device
     with ClockSampler(phys) as clk:
         if flush:
             for _ in range(K):
@@ -348,7 +366,7 @@ def run_workload(name, args, dist, stream_timing=True):
     from paper_1905_02241_b200.parallel import device_checksums, gather_checksums
 
     local = np.concatenate([device_checksums(p.runner, p.dev) for p in pops])
-    table = gather_checksums(local, device=f"cuda:{dist.local}" if dist.pg else None)
+    table = gather_checksums(local, device=dist.tensor_device)
     res = {
         "value": value,
         "checksum_of_checksums": float(np.sum(table[..., 1])),
@@ -401,7 +419,7 @@ def run_column(args, dist):
     graph = rt.capture(s0, lambda: shard.launch(K))
     dist.barrier()
     visible = os.environ.get("CUDA_VISIBLE_DEVICES")
-    phys = int(visible.split(",")[dist.local]) if visible and visible.split(",")[0].isdigit() else dist.local
+    phys = int(visible.split(",")[dist.device]) if visible and visible.split(",")[0].isdigit() else dist.device
     with ClockSampler(phys) as clk:
         ev_a.record(s0)
         graph.launch(s0)
@@ -412,7 +430,7 @@ def run_column(args, dist):
     dist.barrier()
     max_ms = dist.allreduce([ms], "max")[0]
     n_all = dist.allreduce([float(shard.n_instances)], "sum")[0]
-    table = gather_checksums(shard.checksums(), device=f"cuda:{dist.local}" if dist.pg else None)
+    table = gather_checksums(shard.checksums(), device=dist.tensor_device)
     peak, peak_src = _peaks()
     achieved = shard.launch_bytes() / (ms / K / 1e3) / 1e9
     return {
@@ -612,7 +630,7 @@ def main():
         return
     from paper_1905_02241_b200 import runtime as rt
 
-    rt.require_device(dist.local)
+    rt.require_device(dist.device)
     if args.workload == "column":
         res = run_column(args, dist)
         e2e = None

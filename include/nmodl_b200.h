@@ -64,6 +64,7 @@ const char *nmodl_last_error(void);
 int nmodl_abi_version(void);
 int nmodl_device_count(int *out);
 int nmodl_set_device(int dev);
+int nmodl_get_device(int *dev);
 int nmodl_device_info(int dev, int *sm_count, long long *l2_bytes, long long *mem_bytes,
                       int *cc_major, int *cc_minor, char *name, int name_len);
 int nmodl_malloc(void **out, size_t bytes);

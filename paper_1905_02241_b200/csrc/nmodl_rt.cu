@@ -41,6 +41,10 @@ NMODL_API int nmodl_device_count(int* out) {
   CK(cudaGetDeviceCount(out));
   return 0;
 }
+NMODL_API int nmodl_get_device(int* dev) {
+  CK(cudaGetDevice(dev));
+  return 0;
+}
 NMODL_API int nmodl_set_device(int dev) {
   CK(cudaSetDevice(dev));
   return 0;

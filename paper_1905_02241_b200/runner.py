@@ -204,15 +204,14 @@ class CudaRunner:
     """Compiles one mechanism for sm_100a and executes its kernels."""
 
     def __init__(self, layout, jac_mode: str = "exact", *, options: CudaOptions | None = None,
-                 fmad: bool = False, device: int = 0):
+                 fmad: bool = False, device: int | None = None):
         if jac_mode not in ("exact", "fd"):
             raise ValueError("jac_mode must be 'exact' or 'fd'")
         self.layout = layout
         self.ir = from_layout(layout)
         self.jac_mode = jac_mode
         self.flags = 1 if jac_mode == "fd" else 0
-        rt.require_device(device)
-        self.device = device
+        self.device = rt.require_device(device)
         self.options = options or CudaOptions()
         self.mb = build_mechanism(self.ir, self.options, fmad)
         self.abi = self.mb.abi

@@ -39,6 +39,7 @@ _SIGS = {
     "nmodl_abi_version": (C.c_int, []),
     "nmodl_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "nmodl_set_device": (C.c_int, [C.c_int]),
+    "nmodl_get_device": (C.c_int, [C.POINTER(C.c_int)]),
     "nmodl_device_info": (
         C.c_int,
         [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
@@ -120,13 +121,20 @@ def device_count() -> int:
     return n.value if rc == 0 else 0
 
 
-def require_device(dev: int = 0) -> None:
-    if device_count() <= dev:
+def require_device(dev: int | None = None) -> int:
+    """Fail loudly without a device; select `dev` (or keep the current one)."""
+    n = device_count()
+    if n == 0 or (dev is not None and n <= dev):
         raise CudaError(
             "no CUDA device visible: the B200 backend has no CPU fallback "
             "(run on a GPU box, e.g. via gpurun)"
         )
-    check(lib().nmodl_set_device(dev), "cudaSetDevice")
+    if dev is not None:
+        check(lib().nmodl_set_device(dev), "cudaSetDevice")
+        return dev
+    cur = C.c_int(0)
+    check(lib().nmodl_get_device(C.byref(cur)), "cudaGetDevice")
+    return cur.value
 
 
 def device_info(dev: int = 0) -> dict:

@@ -67,6 +67,10 @@ def run(stem, opts, nodes=0, steps=30):
 def main():
     global VARIANTS
     args = sys.argv[1:]
+    if args and args[0] == "--synapse":
+        VARIANTS = [CudaOptions(fast_path=False, tile=t, block=b, min_blocks=m)
+                    for t in (1024, 2048, 4096) for b in (256, 512) for m in (0, 2, 3, 5) if not (b == 512 and m > 2)]
+        args = ["ProbAMPANMDA_EMS"]
     if args and args[0] == "--quick":
         VARIANTS = [CudaOptions(ilp=i, fast_path=f) for f in (False, True) for i in (1, 2)]
         args = args[1:]

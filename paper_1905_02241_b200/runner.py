@@ -163,6 +163,21 @@ class DeviceInstanceData:
         self.prebad: dict[str, int] = {}
         self.nodes: NodeBinding | None = None
 
+    def reorder(self, perm_ptr: int, stream) -> None:
+        """new[k] = old[perm[k]] for every array, into a fresh arena."""
+        names = list(self.names) + ["i_acc", "g_acc"]
+        arena = rt.DeviceBuffer(self.stride * len(names))
+        L = rt.lib()
+        new_ptr = {}
+        for i, name in enumerate(names):
+            dst = arena.ptr + i * self.stride
+            rt.check(L.nmodl_permute(C.c_void_p(self.ptr[name]), C.c_void_p(dst), C.c_void_p(perm_ptr), self.n, 0,
+                                     C.c_void_p(stream.handle)), "permute")
+            new_ptr[name] = dst
+        stream.sync()
+        self.arena = arena  # the old arena returns to the allocator cache
+        self.ptr = new_ptr
+
     # ---- host <-> device ------------------------------------------------------
     def upload_from(self, data, stream) -> None:
         for name in self.names:
@@ -500,13 +515,9 @@ class CudaRunner:
         rt.h2d(nb.tile_segs, tiles.ctypes.data, tiles.nbytes, s)
         nb.n_tiles = len(tiles) - 1
         s.sync()
-        # reorder every instance array into node-sorted order (on the device)
-        tmp = rt.DeviceBuffer(8 * n)
-        for name in list(dev.names) + ["i_acc", "g_acc"]:
-            rt.check(L.nmodl_permute(C.c_void_p(dev.ptr[name]), C.c_void_p(tmp.ptr), C.c_void_p(nb.perm), n, 0,
-                                     C.c_void_p(s.handle)), "permute")
-            rt.d2d(dev.ptr[name], tmp.ptr, 8 * n, s)
-        s.sync()
+        # reorder every instance array into node-sorted order (on the device):
+        # gather into a fresh arena, then retire the old one (no copy back)
+        dev.reorder(nb.perm, s)
         dev.nodes = nb
         # prescan indices refer to instance order; remap to sorted positions
         if dev.prebad:

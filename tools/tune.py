@@ -71,6 +71,9 @@ def main():
         VARIANTS = [CudaOptions(fast_path=False, tile=t, block=b, min_blocks=m)
                     for t in (1024, 2048, 4096) for b in (256, 512) for m in (0, 2, 3, 5) if not (b == 512 and m > 2)]
         args = ["ProbAMPANMDA_EMS"]
+    if args and args[0] == "--hh":
+        VARIANTS = [CudaOptions(ilp=i, fast_path=f, min_blocks=m) for f in (False, True) for i in (1, 2) for m in (0, 3, 4)]
+        args = ["hh_subset"]
     if args and args[0] == "--quick":
         VARIANTS = [CudaOptions(ilp=i, fast_path=f) for f in (False, True) for i in (1, 2)]
         args = args[1:]

@@ -74,6 +74,9 @@ def main():
     if args and args[0] == "--hh":
         VARIANTS = [CudaOptions(ilp=i, fast_path=f, min_blocks=m) for f in (False, True) for i in (1, 2) for m in (0, 3, 4)]
         args = ["hh_subset"]
+    if args and args[0] == "--kinetic":
+        VARIANTS = [CudaOptions(ilp=1, fast_path=f, min_blocks=m) for f in (False, True) for m in (0, 2, 3)]
+        args = ["na6", "cdp5ish"]
     if args and args[0] == "--quick":
         VARIANTS = [CudaOptions(ilp=i, fast_path=f) for f in (False, True) for i in (1, 2)]
         args = args[1:]

@@ -64,9 +64,25 @@ def run(stem, opts, nodes=0, steps=30):
             "ms": ms, "GBps": lb / (ms / 1e3) / 1e9, "inst_steps_per_s": n / (ms / 1e3), "flush": bool(flush)}
 
 
+def grid(spec: str):
+    """'ilp=1,2 fast_path=0,1' -> the CudaOptions cross product."""
+    import itertools
+
+    keys, values = [], []
+    for part in spec.split():
+        k, vs = part.split("=")
+        keys.append(k)
+        values.append([bool(int(v)) if k in ("fast_path", "exp_c", "const_pool", "fast_div") else int(v)
+                       for v in vs.split(",")])
+    return [CudaOptions(**dict(zip(keys, combo))) for combo in itertools.product(*values)]
+
+
 def main():
     global VARIANTS
     args = sys.argv[1:]
+    if args and args[0] == "--grid":
+        VARIANTS = grid(args[1])
+        args = args[2:]
     if args and args[0] == "--synapse":
         VARIANTS = [CudaOptions(fast_path=False, tile=t, block=b, min_blocks=m)
                     for t in (1024, 2048, 4096) for b in (256, 512) for m in (0, 2, 3, 5) if not (b == 512 and m > 2)]

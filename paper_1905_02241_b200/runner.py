@@ -260,6 +260,15 @@ class CudaRunner:
                         self._max_iter.setdefault(kname, int(node.attrs.get("max_iter", NEWTON_MAX_ITER)))
 
     # ---- helpers ----------------------------------------------------------------
+    trace: list | None = None  # set to [] to record (stage, seconds) wall-clock marks
+
+    def _mark(self, stage: str) -> None:
+        if self.trace is not None:
+            import time
+
+            self.stream.sync()
+            self.trace.append((stage, time.perf_counter()))
+
     def _reset_status(self) -> None:
         rt.check(rt.lib().nmodl_status_reset(C.c_void_p(self.status.ptr), C.c_void_p(self.stream.handle)),
                  "status_reset")
@@ -276,10 +285,14 @@ class CudaRunner:
         missing = [s for s in self.abi.slots if s not in data.arrays]
         if missing or "v" not in data.arrays:
             raise _interp_error(f"layout mismatch: instance data lacks {missing or ['v']}")
+        self._mark("upload:start")
         dev = DeviceInstanceData(self, int(data.n), names, data.scalars)
         dev.newton_iters = list(data.newton_iters)
+        self._mark("upload:alloc")
         dev.upload_from(data, self.stream)
+        self._mark("upload:h2d")
         self._prescan(dev)
+        self._mark("upload:prescan")
         return dev
 
     def _prescan(self, dev: DeviceInstanceData) -> None:
@@ -297,10 +310,12 @@ class CudaRunner:
 
     def to_host(self, dev: DeviceInstanceData, data) -> None:
         """Download a device store into `data` (arrays, acc, scalars, newton record)."""
+        self._mark("download:start")
         if dev.nodes is not None:
             self._unpermute_into(dev, data)
         else:
             dev.download_into(data, self.stream)
+        self._mark("download:arrays")
         data.scalars.update(dev.scalars)
         data.newton_iters[:] = dev.newton_iters
 
@@ -444,6 +459,7 @@ class CudaRunner:
         in launch order); otherwise they are allocated from the host arrays."""
         if dev.nodes is not None:
             raise ValueError("nodes already bound")
+        self._mark("bind:start")
         node_index = np.ascontiguousarray(node_index, dtype=np.int32)
         if shared is None:
             node_v = np.ascontiguousarray(node_v, dtype=np.float64)
@@ -469,6 +485,7 @@ class CudaRunner:
                                         C.c_void_p(nb.node_offsets_full), C.c_void_p(scratch), C.c_void_p(nb.perm),
                                         C.c_void_p(nb.rank), C.c_void_p(bad), C.c_void_p(s.handle)),
                  "scatter_layout")
+        self._mark("bind:sort")
         b = np.empty(1, dtype=np.int32)
         rt.d2h(b.ctypes.data, bad, 4, s)
         s.sync()
@@ -496,6 +513,7 @@ class CudaRunner:
         rt.d2h(offsets.ctypes.data, nb.node_offsets_full, offsets.nbytes, s)
         s.sync()
         nb.offsets_host = offsets
+        self._mark("bind:offsets_d2h")
         # segments: the nodes that own at least one instance, in node order;
         # the reduction touches only those (sparse populations such as one
         # channel per soma leave most compartments alone)
@@ -515,9 +533,11 @@ class CudaRunner:
         rt.h2d(nb.tile_segs, tiles.ctypes.data, tiles.nbytes, s)
         nb.n_tiles = len(tiles) - 1
         s.sync()
+        self._mark("bind:segments_tiles")
         # reorder every instance array into node-sorted order (on the device):
         # gather into a fresh arena, then retire the old one (no copy back)
         dev.reorder(nb.perm, s)
+        self._mark("bind:reorder")
         dev.nodes = nb
         # prescan indices refer to instance order; remap to sorted positions
         if dev.prebad:

@@ -101,8 +101,6 @@ def main():
     for stem in stems:
         for opts in VARIANTS:
             nodes = 1_000_000 if stem == "ProbAMPANMDA_EMS" else 0
-            if nodes and opts.ilp == 2:
-                continue
             try:
                 res = run(stem, opts, nodes)
             except Exception as exc:  # noqa: BLE001

@@ -313,12 +313,28 @@ __global__ void k_invert(const long long* __restrict__ perm, long long* __restri
     rank[perm[k]] = k;
 }
 
+// Keep the stream-ordered allocator's pool across synchronisations: with the
+// default release threshold (0) every sync hands the memory back to the
+// driver and the next cudaMallocAsync of CUB's scratch pays for it again.
+static void keep_async_pool() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long threshold = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+  }
+  done = true;
+}
+
 NMODL_API int nmodl_scatter_layout(const int* node_index_dev, long long n, int n_nodes,
                                    unsigned int* counts_dev /* n_nodes */,
                                    long long* offsets_dev /* n_nodes + 1 */,
                                    long long* scratch_dev /* n */, long long* perm_dev /* n */,
                                    long long* rank_dev /* n */, int* bad_dev /* 1 */,
                                    cudaStream_t s) {
+  keep_async_pool();
   CK(cudaMemsetAsync(counts_dev, 0, sizeof(unsigned int) * (size_t)n_nodes, s));
   int big = 0x7fffffff;
   CK(cudaMemcpyAsync(bad_dev, &big, sizeof(int), cudaMemcpyHostToDevice, s));

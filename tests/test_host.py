@@ -246,3 +246,24 @@ def test_constant_division_is_correctly_rounded():
             q = rn(Fr(a) * Fr(y))
             q1 = fma(fma(-c, q, a), y, q)
             assert q1 == rn(Fr(a) / Fr(c)), (c, a)
+
+
+def test_cli_compile_from_ir_and_mod(tmp_path):
+    from paper_1905_02241_b200 import frontend
+    from paper_1905_02241_b200.cli import main
+
+    assert main(["compile", str(ROOT / "fixtures" / "ir" / "na6.json"), "-o", str(tmp_path)]) == 0
+    assert (tmp_path / "na6.cu").is_file() and (tmp_path / "na6.h").is_file()
+    if frontend.modlc_available():
+        assert main(["compile", str(ROOT / "fixtures" / "mod" / "hh_subset.mod"), "-o", str(tmp_path)]) == 0
+        assert (tmp_path / "hh.cu").read_text() == emit_cuda(load_ir("hh_subset")).text
+
+
+def test_cli_rejects_unsupported(tmp_path):
+    from paper_1905_02241_b200.cli import main
+
+    ir = load_ir("corpus_leak")
+    ir.kernels["state_update"] = (Node("Verbatim", (), {"text": "x = 1;"}),)
+    p = tmp_path / "bad.json"
+    p.write_text(ir.to_json())
+    assert main(["compile", str(p), "-o", str(tmp_path)]) == 1

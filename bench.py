@@ -59,6 +59,9 @@ WORKLOADS = {
         "config": BASELINE["configs"][2],
         "mechs": [(m, 20_000_000 // 6) for m in ("NaTs2_t", "K_Pst", "Ca_HVA", "SKv3_1", "Ih", "cadyn")],
         "nodes": 0,
+        # CaDynamics_E2 accumulates the calcium current Ca_HVA writes (same
+        # compartments, same order): its `ica` slot is Ca_HVA's array
+        "couplings": [("cadyn", "ica", "Ca_HVA", "ica")],
     },
     "kinetic1m": {"config": BASELINE["configs"][3], "mechs": [("na6", 1_000_000), ("cdp5ish", 1_000_000)], "nodes": 0},
     # configs[4]: strong scaling -- the column is fixed, cells are split over ranks
@@ -291,6 +294,9 @@ def run_workload(name, args, dist, stream_timing=True):
     pops = [Population(stem, n, w["nodes"], seed, options_for(stem)) for stem, n in w["mechs"]]
     for p in pops:
         p.setup_device()
+    by_stem = {p.stem: p for p in pops}
+    for dst, dslot, src, sslot in w.get("couplings", ()):
+        by_stem[dst].runner.share_slot(by_stem[dst].dev, dslot, by_stem[src].dev, sslot)
     info = rt.device_info(dist.device)
     streams = [p.runner.stream for p in pops]
     working = sum(p.launch_bytes() for p in pops)

@@ -24,7 +24,7 @@ from paper_1905_02241_b200.ir import MechIR  # noqa: E402
 from paper_1905_02241_b200.runner import CudaRunner  # noqa: E402
 from paper_1905_02241_b200.traffic import launch_bytes  # noqa: E402
 
-SIZES = {"hh_subset": 1_000_000, "ProbAMPANMDA_EMS": 10_000_000, "na6": 1_000_000, "cdp5ish": 1_000_000,
+SIZES = {"hh_subset": 1_000_000, "ProbAMPANMDA_EMS": 10_000_000, "na6": 1_000_000, "cdp5ish": 1_000_000, "cadyn": 3_333_333, "SKv3_1": 3_333_333, "Ih": 3_333_333,
          "NaTs2_t": 3_333_333, "K_Pst": 3_333_333, "Ca_HVA": 3_333_333}
 SHAPES = [dict(ilp=1), dict(ilp=2), dict(ilp=1, min_blocks=4), dict(ilp=1, min_blocks=3), dict(ilp=2, min_blocks=3)]
 CODEGEN = [dict(fast_path=False), dict()]
@@ -72,7 +72,7 @@ def grid(spec: str):
     for part in spec.split():
         k, vs = part.split("=")
         keys.append(k)
-        values.append([bool(int(v)) if k in ("fast_path", "exp_c", "const_pool", "fast_div", "const_div", "exp_inline") else int(v)
+        values.append([bool(int(v)) if k in ("fast_path", "exp_c", "const_pool", "fast_div", "const_div", "exp_inline", "stream_hints") else int(v)
                        for v in vs.split(",")])
     return [CudaOptions(**dict(zip(keys, combo))) for combo in itertools.product(*values)]
 

@@ -17,7 +17,7 @@
  *     (<mech>_data *md)`                                   codegen.py:56-61,450-455
  *   - emitted instance struct `<mech>_data`                codegen.py:425-437
  *   - `modlc_lu_solve(a, b, x, k)`                         codegen.py:540-565
- *     (now a register template, nmodl::lu_solve<K>, inside the kernels)
+ *     (now straight-line register code emitted per solve by the printer)
  *   - `Runner.run_kernel(data, kernel_name, steps)`        interp.py:456-471
  *     (the Python CudaRunner calls the entry points below through ctypes)
  *   - `InterpError` conditions                             interp.py:285,406,538,619

@@ -433,6 +433,21 @@ def run_column(args, dist):
         ev_b.sync()
     ms = ev_a.elapsed_ms(ev_b)
     shard.check()
+    # per-population launch durations (separate pass, events between kernels)
+    from paper_1905_02241_b200.column import LAUNCH_ORDER
+
+    pev = {m: (rt.Event(), rt.Event()) for m in LAUNCH_ORDER}
+    per_pop = {m: 0.0 for m in LAUNCH_ORDER}
+    reps = min(K, 10)
+    for _ in range(reps):
+        for m in LAUNCH_ORDER:
+            pev[m][0].record(s0)
+            shard.runners[m].launch(shard.devs[m], "step_nodes", 1)
+            pev[m][1].record(s0)
+        s0.sync()
+        for m in LAUNCH_ORDER:
+            per_pop[m] += pev[m][0].elapsed_ms(pev[m][1]) / reps
+    shard.check()
     dist.barrier()
     max_ms = dist.allreduce([ms], "max")[0]
     n_all = dist.allreduce([float(shard.n_instances)], "sum")[0]
@@ -451,7 +466,8 @@ def run_column(args, dist):
                      "bytes_per_launch": shard.launch_bytes()},
         "checksum_of_checksums": float(np.sum(table[..., 1])),
         "cells_per_rank": [int(b) for b in np.diff(bounds)],
-        "per_mechanism": {m: {"instances": shard.devs[m].n} for m in shard.devs},
+        "per_mechanism": {m: {"instances": shard.devs[m].n, "ms_per_launch": per_pop[m],
+                              "segments": shard.devs[m].nodes.n_segs} for m in shard.devs},
     }
 
 

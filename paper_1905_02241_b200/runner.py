@@ -525,8 +525,13 @@ class CudaRunner:
         rt.h2d(nb.seg_node, seg_node.ctypes.data, seg_node.nbytes, s)
         rt.h2d(nb.seg_offsets, seg_off.ctypes.data, seg_off.nbytes, s)
         # target 3/4 of the shared-memory capacity so a tile rarely spills to
-        # the global-memory reduction path when a segment straddles a boundary
-        T = tile or max(1, (3 * self.options.tile) // 4)
+        # the global-memory reduction path when a segment straddles a boundary,
+        # but keep >= 4 tiles per SM so small populations still fill the GPU
+        if tile is None:
+            sms = rt.device_info(self.device)["sm_count"]
+            T = max(64, min((3 * self.options.tile) // 4, -(-n // (4 * sms))))
+        else:
+            T = tile
         tiles = tile_nodes_for(seg_off, T)
         nb.tile_segs_host = tiles
         nb.tile_segs = nb.alloc(8 * len(tiles))

@@ -520,6 +520,7 @@ class CudaRunner:
         seg_node = np.flatnonzero(np.diff(offsets)).astype(np.int32)
         seg_off = np.concatenate([offsets[seg_node], [n]]).astype(np.int64)
         nb.n_segs = len(seg_node)
+        nb.seg_unique = 1 if nb.n_segs == n else 0  # every occupied node holds exactly one instance
         nb.seg_node = nb.alloc(4 * max(1, len(seg_node)))
         nb.seg_offsets = nb.alloc(8 * len(seg_off))
         rt.h2d(nb.seg_node, seg_node.ctypes.data, seg_node.nbytes, s)

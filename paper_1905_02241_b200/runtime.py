@@ -8,6 +8,7 @@ device is visible -- there is no CPU fallback anywhere on the product path.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import threading
 
 from .build import RUNTIME_SO, build_runtime
@@ -137,6 +138,7 @@ def require_device(dev: int | None = None) -> int:
     return cur.value
 
 
+@functools.lru_cache(maxsize=None)
 def device_info(dev: int = 0) -> dict:
     sm, l2, mem, ma, mi = C.c_int(), C.c_longlong(), C.c_longlong(), C.c_int(), C.c_int()
     name = C.create_string_buffer(128)

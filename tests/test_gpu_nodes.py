@@ -74,3 +74,23 @@ def test_scatter_arithmetic_bit_exact():
     N.scatter(rhs_ref, d_ref, idx, gpu.acc["i_acc"], gpu.acc["g_acc"])
     np.testing.assert_array_equal(rhs_gpu, rhs_ref)
     np.testing.assert_array_equal(d_gpu, d_ref)
+
+
+@pytest.mark.parametrize("stem", ["Ih", "hh_subset", "ProbAMPANMDA_EMS"])
+def test_one_instance_per_node_path(stem):
+    """node_index a permutation (density mechanisms: <= 1 instance per
+    compartment): the conflict-free direct-update path, same results."""
+    from paper_1905_02241_b200.runner import CudaRunner, simulate_nodes
+
+    ir = load_ir(stem)
+    n = 7001
+    idx = np.random.default_rng(5).permutation(n).astype(np.int32)
+    nv = np.random.default_rng(6).uniform(-80, 40, n)
+    rhs0, d0 = np.linspace(-1, 1, n), np.linspace(1, 2, n)
+    ref, rhs_ref, d_ref = N.simulate_nodes(ir, O.init(ir, n, 2), 40, idx, nv, rhs0, d0)
+    runner = CudaRunner(ir)
+    gpu, rhs_gpu, d_gpu = simulate_nodes(ir, O.init(ir, n, 2), 40, idx, nv, rhs0.copy(), d0.copy(), runner=runner)
+    dev, where = parity(ir, ref, gpu)
+    assert dev <= TOL, (where, dev)
+    np.testing.assert_allclose(rhs_gpu, rhs_ref, rtol=1e-9, atol=0)
+    np.testing.assert_allclose(d_gpu, d_ref, rtol=1e-9, atol=0)

@@ -436,17 +436,18 @@ def run_column(args, dist):
     # per-population launch durations (separate pass, events between kernels)
     from paper_1905_02241_b200.column import LAUNCH_ORDER
 
-    pev = {m: (rt.Event(), rt.Event()) for m in LAUNCH_ORDER}
-    per_pop = {m: 0.0 for m in LAUNCH_ORDER}
-    reps = min(K, 10)
-    for _ in range(reps):
-        for m in LAUNCH_ORDER:
-            pev[m][0].record(s0)
-            shard.runners[m].launch(shard.devs[m], "step_nodes", 1)
-            pev[m][1].record(s0)
-        s0.sync()
-        for m in LAUNCH_ORDER:
-            per_pop[m] += pev[m][0].elapsed_ms(pev[m][1]) / reps
+    # (each population's launches captured in its own graph, so host launch
+    # latency does not pollute the small populations' times)
+    per_pop = {}
+    reps = 10
+    for m in LAUNCH_ORDER:
+        g = rt.capture(s0, lambda m=m: shard.runners[m].launch(shard.devs[m], "step_nodes", reps))
+        a, b = rt.Event(), rt.Event()
+        a.record(s0)
+        g.launch(s0)
+        b.record(s0)
+        b.sync()
+        per_pop[m] = a.elapsed_ms(b) / reps
     shard.check()
     dist.barrier()
     max_ms = dist.allreduce([ms], "max")[0]

@@ -320,29 +320,29 @@ class CudaRunner:
         data.newton_iters[:] = dev.newton_iters
 
     def _struct(self, dev: DeviceInstanceData, newton_rec=0):
-        md = self.Struct()
+        """The `<mech>_data` argument block for `dev` (positional build: this
+        runs once per launch call on the host)."""
+        nb = dev.nodes
+        vals = []
         for f in self.abi.fields:
-            if f.role == "count":
-                setattr(md, f.name, dev.n)
-            elif f.role == "status":
-                setattr(md, f.name, self.status.ptr)
-            elif f.role == "newton":
-                setattr(md, f.name, newton_rec or None)
-            elif f.role == "scalars_rw":
-                setattr(md, f.name, dev.scalars_rw.ptr)
-            elif f.role == "scalar":
+            role = f.role
+            if role == "slot" or role == "v" or role == "acc":
+                vals.append(dev.ptr[f.key])
+            elif role == "scalar":
                 if f.key not in dev.scalars:
                     raise _interp_error(f"unbound name {f.key!r}")
-                setattr(md, f.name, float(dev.scalars[f.key]))
-            elif f.role in ("v", "acc", "slot"):
-                setattr(md, f.name, dev.ptr[f.key])
-            elif f.role == "node":
-                nb = dev.nodes
-                if nb is None:
-                    setattr(md, f.name, 0 if f.ctype == "i64" else None)
-                else:
-                    setattr(md, f.name, getattr(nb, f.key))
-        return md
+                vals.append(float(dev.scalars[f.key]))
+            elif role == "count":
+                vals.append(dev.n)
+            elif role == "status":
+                vals.append(self.status.ptr)
+            elif role == "newton":
+                vals.append(newton_rec or None)
+            elif role == "scalars_rw":
+                vals.append(dev.scalars_rw.ptr)
+            elif role == "node":
+                vals.append((0 if f.ctype == "i64" else None) if nb is None else getattr(nb, f.key))
+        return self.Struct(*vals)
 
     def _sync_scalars_in(self, dev) -> None:
         rw = self.abi.rw_scalars

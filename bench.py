@@ -275,6 +275,10 @@ class Population:
                                              C.c_void_p(self.dev.ptr["v"]), self.n, C.c_void_p(r.stream.handle)),
                      "gather_v")
         r.run_kernel(self.dev, "initialize", 1)
+        # the store is resident now: drop the host copy (8 ranks x GBs of numpy otherwise)
+        self.data = None
+        if self.n_nodes:
+            self.node_index = self.node_v = None
 
     def launch(self, steps=1):
         self.runner.launch(self.dev, self.kernel, steps)

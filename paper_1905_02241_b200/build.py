@@ -98,10 +98,11 @@ class MechBuild:
         self.text = text
 
 
-def build_mechanism(layout, options: CudaOptions | None = None, fmad: bool = False,
+def build_mechanism(layout, options: CudaOptions | None = None, fmad: bool | None = None,
                     force: bool = False) -> MechBuild:
     """emit_cuda + nvcc -> content-addressed shared object."""
     options = options or CudaOptions()
+    fmad = options.fmad if fmad is None else fmad
     printer = CudaPrinter(layout, options)
     text = printer.emit_unit()
     abi = printer._abi
@@ -125,7 +126,7 @@ def build_mechanism(layout, options: CudaOptions | None = None, fmad: bool = Fal
     return MechBuild(so, cu, abi, printer.mech, text)
 
 
-def build_many(layouts, options: CudaOptions | None = None, fmad: bool = False,
+def build_many(layouts, options: CudaOptions | None = None, fmad: bool | None = None,
                jobs: int | None = None) -> list[MechBuild]:
     jobs = jobs or min(8, os.cpu_count() or 4)
     with ThreadPoolExecutor(jobs) as pool:

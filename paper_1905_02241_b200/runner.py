@@ -219,7 +219,7 @@ class CudaRunner:
     """Compiles one mechanism for sm_100a and executes its kernels."""
 
     def __init__(self, layout, jac_mode: str = "exact", *, options: CudaOptions | None = None,
-                 fmad: bool = False, device: int | None = None):
+                 fmad: bool | None = None, device: int | None = None):
         if jac_mode not in ("exact", "fd"):
             raise ValueError("jac_mode must be 'exact' or 'fd'")
         self.layout = layout

@@ -94,3 +94,21 @@ def test_one_instance_per_node_path(stem):
     assert dev <= TOL, (where, dev)
     np.testing.assert_allclose(rhs_gpu, rhs_ref, rtol=1e-9, atol=0)
     np.testing.assert_allclose(d_gpu, d_ref, rtol=1e-9, atol=0)
+
+
+@pytest.mark.parametrize("n,n_nodes,tile", [(20000, 2000, 512), (6000, 3, 512), (9000, 4000, 256), (777, 50, 128)])
+def test_tma_bulk_node_kernel_matches_oracle(n, n_nodes, tile):
+    """Double-buffered cp.async.bulk staging (including oversized tiles that
+    fall back to global loads and odd/unaligned tile starts)."""
+    from paper_1905_02241_b200.codegen_cuda import CudaOptions
+    from paper_1905_02241_b200.runner import CudaRunner, simulate_nodes
+
+    ir = load_ir("ProbAMPANMDA_EMS")
+    idx, nv = _inputs(n, n_nodes, 4)
+    ref, rhs_ref, d_ref = N.simulate_nodes(ir, O.init(ir, n, 8), 60, idx, nv)
+    runner = CudaRunner(ir, options=CudaOptions(bulk=True, tile=tile, fast_path=False))
+    gpu, rhs_gpu, d_gpu = simulate_nodes(ir, O.init(ir, n, 8), 60, idx, nv, runner=runner)
+    dev, where = parity(ir, ref, gpu)
+    assert dev <= TOL, (where, dev)
+    np.testing.assert_allclose(rhs_gpu, rhs_ref, rtol=1e-9, atol=0)
+    np.testing.assert_allclose(d_gpu, d_ref, rtol=1e-9, atol=0)

@@ -1,0 +1,149 @@
+"""Per-kernel operation census and roofline classification for B200.
+
+Restates the reference's static analysis (modlc/analysis.py:77-147 `_Census`,
+:158-265 `_Traffic`/`profile_kernel`) for the fused CUDA step and prices it
+on B200: the census counts the per-instance operations of nrn_state +
+nrn_cur as generated (numeric conductance doubles the current body,
+modlc/analysis.py:243-250; solver nodes count one Newton iteration / one LU),
+the traffic is the generated kernel's own load/store set (traffic.py), and
+the FP64 cost uses the instruction counts of the sequences actually emitted
+(SASS-derived: exp 16 FP64 ops, IEEE division 8 + MUFU, literal division 3).
+
+`roofline(ir)` returns both times for one instance-step and which one binds:
+    t_hbm  = bytes / HBM bandwidth        (MEASURED_PEAKS.json hbm_gbs)
+    t_fp64 = FP64 ops / FP64 rate         (148 SM x 64 FP64 lanes x clock)
+"""
+
+from __future__ import annotations
+
+import math
+from collections import Counter
+
+from .codegen_cuda import CudaPrinter
+from .ir import from_layout, iter_nodes, newton_parts
+from .traffic import bytes_per_instance
+
+# FP64 pipe operations per emitted operation (from the sm_100a SASS of the
+# generated code: tools/ncu_opcodes.py on profiles/r01/prof_r1f_*).
+FP64_COST = {"exp": 16, "log": 22, "sqrt": 10, "pow": 60, "div": 8, "div_const": 3, "rcp": 6,
+             "add": 1, "sub": 1, "mul": 1, "neg": 0, "cmp": 1, "fabs": 0, "ipow": 2}
+FP64_LANES_PER_SM = 64
+SM_COUNT = 148
+
+
+def _census_expr(node, out: Counter, fns) -> None:
+    for n in iter_nodes(node):
+        k = n.kind
+        if k == "Binary":
+            op = n.attrs["op"]
+            if op == "/":
+                lhs, rhs = n.children
+                if rhs.kind == "Number":
+                    out["div_const"] += 1
+                elif lhs.kind == "Number" and lhs.attrs["value"] == 1.0:
+                    out["rcp"] += 1
+                else:
+                    out["div"] += 1
+            elif op == "^":
+                r = n.children[1]
+                if r.kind == "Number" and r.attrs["value"] in (2.0, 3.0, 4.0):
+                    out["ipow"] += 1
+                else:
+                    out["pow"] += 1
+            elif op in ("+",):
+                out["add"] += 1
+            elif op == "-":
+                out["sub"] += 1
+            elif op == "*":
+                out["mul"] += 1
+            elif op in ("<", "<=", ">", ">=", "==", "!="):
+                out["cmp"] += 1
+        elif k == "Unary" and n.attrs["op"] == "-":
+            out["neg"] += 1
+        elif k == "Call":
+            name = n.attrs["name"]
+            if name in ("exp", "log", "sqrt", "pow", "fabs"):
+                out[name] += 1
+            elif name in fns:
+                for s in fns[name].children[-1].children:
+                    _census_expr(s, out, fns)
+
+
+def census(layout) -> Counter:
+    """Operations per instance-step of the fused state + current kernel."""
+    ir = from_layout(layout)
+    out: Counter = Counter()
+    for kname in ("state_update", "current_update"):
+        mult = 2 if (kname == "current_update" and ir.currents and not ir.analytic_conductance) else 1
+        c: Counter = Counter()
+        for s in ir.kernels.get(kname, ()):
+            if s.kind == "NewtonSolveNode":
+                res, jac = newton_parts(s)
+                for e in res + [x for row in jac for x in row]:
+                    _census_expr(e, c, ir.functions)
+                k = s.attrs["n"]
+                c["div"] += k  # one LU / adjugate division per unknown
+                c["mul"] += k ** 3 // 3
+                c["sub"] += k ** 3 // 3
+            elif s.kind == "LinearSolveNode":
+                _census_expr(s, c, ir.functions)
+                k = s.attrs["n"]
+                c["div"] += k * (k + 1) // 2
+                c["mul"] += k ** 3 // 3
+                c["sub"] += k ** 3 // 3
+            else:
+                _census_expr(s, c, ir.functions)
+        for key, v in c.items():
+            out[key] += v * mult
+    return out
+
+
+def fp64_ops(layout) -> int:
+    return sum(FP64_COST.get(k, 1) * v for k, v in census(layout).items())
+
+
+def roofline(layout, hbm_gbs: float = 6539.2, clock_ghz: float = 1.965, kernel: str = "step") -> dict:
+    """Per instance-step: bytes, FP64 ops, time at the HBM and FP64 roofs."""
+    ir = from_layout(layout)
+    p = CudaPrinter(ir)
+    p.emit_unit()
+    b = bytes_per_instance(p._abi, kernel)
+    f = fp64_ops(ir)
+    fp64_rate = SM_COUNT * FP64_LANES_PER_SM * clock_ghz * 1e9
+    t_hbm = b / (hbm_gbs * 1e9)
+    t_fp = f / fp64_rate
+    return {
+        "mechanism": ir.mechanism,
+        "bytes_per_instance": b,
+        "fp64_ops_per_instance": f,
+        "ops": dict(census(ir)),
+        "t_hbm_ns": t_hbm * 1e9 * 1e3 / 1e3,
+        "t_fp64_ns": t_fp * 1e9,
+        "bound": "hbm" if t_hbm >= t_fp else "fp64",
+        "fp64_per_byte": f / max(b, 1),
+        "ridge_fp64_per_byte": fp64_rate / (hbm_gbs * 1e9),
+        "max_hbm_fraction_at_fp64_roof": min(1.0, t_hbm / t_fp) if t_fp > 0 else 1.0,
+    }
+
+
+def table(stems_and_layouts) -> str:
+    rows = ["| mechanism | B/inst-step | FP64 ops/inst-step | FP64 ops/B | bound | max HBM fraction |",
+            "|---|---|---|---|---|---|"]
+    for name, lay in stems_and_layouts:
+        r = roofline(lay)
+        rows.append(f"| {name} | {r['bytes_per_instance']} | {r['fp64_ops_per_instance']} | "
+                    f"{r['fp64_per_byte']:.2f} | {r['bound']} | {min(1.0, r['max_hbm_fraction_at_fp64_roof']):.0%} |")
+    return "\n".join(rows)
+
+
+if __name__ == "__main__":  # pragma: no cover
+    import sys
+    from pathlib import Path
+
+    from .ir import MechIR
+
+    root = Path(__file__).resolve().parent.parent / "fixtures" / "ir"
+    stems = sys.argv[1:] or ["ProbAMPANMDA_EMS", "hh_subset", "NaTs2_t", "K_Pst", "Ca_HVA", "SKv3_1", "Ih",
+                             "cadyn", "na6", "cdp5ish"]
+    print(table([(s, MechIR.load(root / f"{s}.json")) for s in stems]))
+    _ = math

@@ -267,3 +267,16 @@ def test_cli_rejects_unsupported(tmp_path):
     p = tmp_path / "bad.json"
     p.write_text(ir.to_json())
     assert main(["compile", str(p), "-o", str(tmp_path)]) == 1
+
+
+def test_census_counts_match_the_mechanism():
+    """hh: 9 exp per instance-step (6 rates + 3 cnexp), x^3/x^4 as products,
+    numeric-conductance bodies counted twice (modlc/analysis.py:243-250)."""
+    from paper_1905_02241_b200.analysis import census, roofline
+
+    c = census(load_ir("hh_subset"))
+    assert c["exp"] == 9 and c["pow"] == 1 and c["ipow"] == 2  # q10 stays a (hoisted) pow
+    syn = census(load_ir("ProbAMPANMDA_EMS"))
+    assert syn["exp"] == 4 + 2  # 4 cnexp decays + Mg block at v and v+h
+    r = roofline(load_ir("ProbAMPANMDA_EMS"))
+    assert r["bound"] == "hbm" and r["bytes_per_instance"] == 152

@@ -597,12 +597,44 @@ def cpu_reference(name, target_s=10.0, max_n=2_000_000, steps_cap=200):
         "unit": UNIT,
         "cores": threads,
         "kind": "reference",
+        "numpy_oracle": numpy_oracle_rate(name),
         "sample": "reference-emitted scalar C (modlc.codegen.emit_scalar, count field renamed), gcc -O3 "
                   "-march=native, contiguous shards per thread, accumulators zeroed per step; "
                   + "; ".join(per_mech)
                   + ("; no node_index scatter (the reference has none)" if w["nodes"] else ""),
         "cpu": _cpu_model(),
     }
+
+
+def numpy_oracle_rate(name, n=65536, budget_s=4.0):
+    """SURVEY.md §8(d) CPU leg 2: the reference's numpy runtime semantics
+    (`modlc.interp.Runner`, restated bit-exactly in oracle/interp_np.py),
+    single-threaded by design, on a 65,536-instance prefix of each mechanism;
+    the population step is the n-weighted sum of the per-mechanism times."""
+    from oracle import interp_np as O
+    from paper_1905_02241_b200.ir import MechIR
+
+    w = WORKLOADS[name]
+    if not w["mechs"]:
+        return None
+    total_s, total_n, parts = 0.0, 0, []
+    for stem, n_full in w["mechs"]:
+        ir = MechIR.load(ROOT / "fixtures" / "ir" / f"{stem}.json")
+        data = O.init(ir, n, 42)
+        runner = O.OracleRunner(ir)
+        runner.run_kernel(data, "initialize", 1)
+        steps, dt = 0, 0.0
+        t0 = time.perf_counter()
+        while dt < budget_s / len(w["mechs"]) or steps < 2:
+            runner.run_kernel(data, "state_update", 1)
+            runner.run_kernel(data, "current_update", 1)
+            steps += 1
+            dt = time.perf_counter() - t0
+        total_s += dt / steps * (n_full / n)
+        total_n += n_full
+        parts.append(f"{stem}: {n} x {steps} steps in {dt:.2f}s")
+    return {"value": total_n / total_s, "unit": UNIT, "cores": 1,
+            "sample": "oracle/interp_np.py (numpy restatement of modlc.interp.Runner), single thread; " + "; ".join(parts)}
 
 
 def reference_arm(name, K, W, budget_s=60.0):

@@ -160,6 +160,11 @@ class DeviceInstanceData:
         self.ptr["g_acc"] = self.arena.ptr + (len(self.names) + 1) * stride
         nrw = max(1, len(runner.abi.rw_scalars))
         self.scalars_rw = rt.DeviceBuffer(8 * nrw)
+        # deferred-instance list + ping-pong counters (CudaOptions.defer)
+        self.defer_list = rt.DeviceBuffer(4 * max(n, 1)) if runner.options.defer else None
+        self.defer_count = rt.DeviceBuffer(8) if runner.options.defer else None
+        if self.defer_count is not None:
+            rt.memset(self.defer_count.ptr, 0, 8, runner.stream)
         self.prebad: dict[str, int] = {}
         self.nodes: NodeBinding | None = None
 
@@ -342,6 +347,12 @@ class CudaRunner:
                 vals.append(dev.scalars_rw.ptr)
             elif role == "node":
                 vals.append((0 if f.ctype == "i64" else None) if nb is None else getattr(nb, f.key))
+            elif role == "defer":
+                if f.key == "defer_par":
+                    vals.append(0)
+                else:
+                    buf = getattr(dev, f.key, None)
+                    vals.append(buf.ptr if buf is not None else None)
         return self.Struct(*vals)
 
     def _sync_scalars_in(self, dev) -> None:
@@ -366,6 +377,9 @@ class CudaRunner:
         if kernel_name == "step_nodes" and dev.nodes is None:
             raise ValueError("step_nodes needs bind_nodes() first")
         md = self._struct(dev, newton_rec)
+        if getattr(dev, "defer_count", None) is not None:
+            # an aborted launch can leave a count behind; start every call clean
+            rt.memset(dev.defer_count.ptr, 0, 8, self.stream)
         rc = self.entry[kernel_name](C.byref(md), int(steps), C.c_void_p(self.stream.handle), self.flags)
         rt.check(rc, f"launch {self.mb.symbol}_{kernel_name}")
 

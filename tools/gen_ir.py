@@ -38,6 +38,9 @@ def main() -> int:
     jobs.append((cat, "corpus_cat.pade", {"pade": True}))
     hh = ROOT / "fixtures" / "mod" / "hh_subset.mod"
     jobs.append((hh, "hh_subset.nopass", {"passes": ()}))
+    # Pade (2+x)/(2-x) cnexp update (modlc/odes.py:414-434): the exp-cost lever
+    jobs.append((hh, "hh_subset.pade", {"pade": True}))
+    jobs.append((ROOT / "fixtures" / "mod" / "NaTs2_t.mod", "NaTs2_t.pade", {"pade": True}))
     three = next(p for p in corpus_files() if p.stem == "threestate")
     jobs.append((three, "corpus_threestate.nocse", {"use_cse": False}))
     written = 0

@@ -542,18 +542,26 @@ def e2e_measure(name, dist, calls=2, timesteps=1000):
 
 
 def _h2d(job):
+    """Bytes the public call copies host->device: the whole store (v excepted
+    in node mode: it is gathered from the node voltages), node_index, node_v."""
     ir, runner, data, extra, _, n = job
-    b = sum(a.nbytes for a in data.arrays.values()) + sum(a.nbytes for a in data.acc.values())
+    b = sum(a.nbytes for k, a in data.arrays.items() if not (extra is not None and k == "v"))
+    b += sum(a.nbytes for a in data.acc.values())
     if extra is not None:
         b += extra[0].nbytes + extra[1].nbytes
     return b
 
 
 def _d2h(job):
+    """Bytes copied back: the arrays a launch may write (states, assigned,
+    currents, accumulators; v in node mode) and the node rhs/d arrays."""
     ir, runner, data, extra, _, n = job
-    b = sum(a.nbytes for a in data.arrays.values()) + sum(a.nbytes for a in data.acc.values())
+    written = runner._writes["initialize"] | runner._writes["step_nodes" if extra is not None else "step"]
     if extra is not None:
-        b += 3 * extra[1].nbytes + 2 * 8 * n + 4 * n
+        written = written | {"v"}
+    b = sum(8 * n for k in list(data.arrays) + ["i_acc", "g_acc"] if k in written)
+    if extra is not None:
+        b += 2 * extra[1].nbytes
     return b
 
 
@@ -788,7 +796,7 @@ def main():
             "data": "synthetic (modlc.interp.init-format seeded instance store; random node_index)",
             "config": config,
             "roofline": res["roofline"],
-            "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu")},
+            "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu", "numpy_oracle")},
             "e2e": e2e,
             "gpu_launches": res["gpu_launches"],
             "clocks": res["clocks"],

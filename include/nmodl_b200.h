@@ -108,6 +108,12 @@ int nmodl_l2_flush(double *buf, long long n_doubles, nmodl_stream_t s);
 int nmodl_scatter_layout(const int *node_index_dev, long long n, int n_nodes, unsigned int *counts_dev,
                          long long *offsets_dev, long long *scratch_dev, long long *perm_dev,
                          long long *rank_dev, int *bad_dev, nmodl_stream_t s);
+/* occupied node segments (seg_node, seg_off = offsets[seg_node] ++ [n]) and
+ * CTA tiles of whole segments, ~`tile` instances each; counts_dev[0] =
+ * n_segs, counts_dev[1] = tile boundaries (n_tiles + 1).  Builder-defined. */
+int nmodl_node_segments(const long long *offsets_dev, int n_nodes, long long n, long long tile,
+                        int *seg_node_dev, long long *seg_off_dev, long long *tiles_dev, long long *counts_dev,
+                        nmodl_stream_t s);
 int nmodl_permute(const double *src, double *dst, const long long *perm, long long n, int inverse,
                   nmodl_stream_t s);
 int nmodl_permute_i32(const int *src, int *dst, const long long *perm, long long n, nmodl_stream_t s);

@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
@@ -369,6 +371,92 @@ NMODL_API int nmodl_scatter_layout(const int* node_index_dev, long long n, int n
   CK(cudaFreeAsync(keys_out, s));
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+// occupied segments and CTA tiles of a node layout, on the device
+// (runner.bind_nodes; the host restatement is runner.tile_nodes_for):
+//   seg_node = nodes k with offsets[k+1] > offsets[k], ascending
+//   seg_off  = offsets[seg_node] ++ [n]
+//   tiles    = unique([0] ++ lower_bound(seg_off[:-1], m*T for m*T < max(n,1)) ++ [n_segs])
+__global__ void k_seg_flags(const long long* __restrict__ offsets, int n_nodes, unsigned char* __restrict__ flag) {
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n_nodes;
+       k += (long long)gridDim.x * blockDim.x)
+    flag[k] = offsets[k + 1] > offsets[k] ? 1 : 0;
+}
+__global__ void k_seg_offsets(const long long* __restrict__ offsets, const int* __restrict__ seg_node,
+                              const long long* __restrict__ n_segs_dev, long long n, long long* __restrict__ seg_off) {
+  const long long m = *n_segs_dev;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j <= m;
+       j += (long long)gridDim.x * blockDim.x)
+    seg_off[j] = j < m ? offsets[seg_node[j]] : n;
+}
+__global__ void k_tile_marks(const long long* __restrict__ seg_off, const long long* __restrict__ n_segs_dev,
+                             long long n_marks, long long tile, long long* __restrict__ cand,
+                             unsigned char* __restrict__ flag) {
+  const long long m = *n_segs_dev;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t <= n_marks;
+       t += (long long)gridDim.x * blockDim.x) {
+    long long c;
+    if (t == n_marks) {
+      c = m;
+    } else {  // first segment whose offset is >= t * tile
+      const long long key = t * tile;
+      long long lo = 0, hi = m;
+      while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (seg_off[mid] < key) lo = mid + 1; else hi = mid;
+      }
+      c = lo;
+    }
+    cand[t] = c;
+  }
+}
+__global__ void k_tile_flags(const long long* __restrict__ cand, long long n_cand, unsigned char* __restrict__ flag) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n_cand;
+       t += (long long)gridDim.x * blockDim.x)
+    flag[t] = (t == 0 || cand[t] != cand[t - 1]) ? 1 : 0;
+}
+
+static int grid_for(long long n) {
+  long long b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  return b < 1 ? 1 : (int)b;
+}
+
+NMODL_API int nmodl_node_segments(const long long* offsets_dev /* n_nodes + 1 */, int n_nodes, long long n,
+                                  long long tile, int* seg_node_dev /* n_nodes */,
+                                  long long* seg_off_dev /* n_nodes + 1 */,
+                                  long long* tiles_dev /* n_marks + 2, n_marks = ceil(max(n,1)/tile) */,
+                                  long long* counts_dev /* 2: n_segs, n_tiles + 1 */, cudaStream_t s) {
+  keep_async_pool();
+  if (tile < 1) return (int)cudaErrorInvalidValue;
+  const long long n_marks = ((n > 0 ? n : 1) + tile - 1) / tile;
+  // marks start at 0, so cand[0] = 0 and the leading [0] of the restatement is implicit
+  const long long n_cand = n_marks + 1;
+  unsigned char* flag = nullptr;
+  long long* cand = nullptr;
+  const long long flag_len = (n_nodes > n_cand ? (long long)n_nodes : n_cand) + 1;
+  CK(cudaMallocAsync((void**)&flag, (size_t)flag_len, s));
+  CK(cudaMallocAsync((void**)&cand, sizeof(long long) * (size_t)n_cand, s));
+  k_seg_flags<<<grid_for(n_nodes), 256, 0, s>>>(offsets_dev, n_nodes, flag);
+  size_t bytes = 0, b2 = 0;
+  CK(cub::DeviceSelect::Flagged(nullptr, bytes, cub::CountingInputIterator<int>(0), flag, seg_node_dev,
+                                counts_dev, n_nodes, s));
+  CK(cub::DeviceSelect::Flagged(nullptr, b2, cand, flag, tiles_dev, counts_dev + 1, n_cand, s));
+  if (b2 > bytes) bytes = b2;
+  void* tmp = nullptr;
+  CK(cudaMallocAsync(&tmp, bytes ? bytes : 16, s));
+  CK(cub::DeviceSelect::Flagged(tmp, bytes, cub::CountingInputIterator<int>(0), flag, seg_node_dev,
+                                counts_dev, n_nodes, s));
+  k_seg_offsets<<<grid_for((long long)n_nodes + 1), 256, 0, s>>>(offsets_dev, seg_node_dev, counts_dev, n, seg_off_dev);
+  k_tile_marks<<<grid_for(n_cand), 256, 0, s>>>(seg_off_dev, counts_dev, n_marks, tile, cand, flag);
+  k_tile_flags<<<grid_for(n_cand), 256, 0, s>>>(cand, n_cand, flag);
+  CK(cub::DeviceSelect::Flagged(tmp, bytes, cand, flag, tiles_dev, counts_dev + 1, n_cand, s));
+  CK(cudaFreeAsync(tmp, s));
+  CK(cudaFreeAsync(cand, s));
+  CK(cudaFreeAsync(flag, s));
+  CK(cudaGetLastError());
   return 0;
 }
 

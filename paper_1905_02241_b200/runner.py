@@ -111,6 +111,27 @@ class NodeBinding:
     def perm_host(self):
         return self.host_array("perm", self.stream)
 
+    def _host_i64(self, name, ptr, count):
+        cache = self.__dict__.setdefault("_host", {})
+        if name not in cache:
+            arr = np.empty(count, dtype=np.int64)
+            rt.d2h(arr.ctypes.data, ptr, arr.nbytes, self.stream)
+            self.stream.sync()
+            cache[name] = arr
+        return cache[name]
+
+    @property
+    def offsets_host(self):
+        return self._host_i64("offsets", self.node_offsets_full, self.n_nodes + 1)
+
+    @property
+    def tile_segs_host(self):
+        return self._host_i64("tile_segs", self.tile_segs, self.n_tiles + 1)
+
+    @property
+    def seg_offsets_host(self):
+        return self._host_i64("seg_offsets", self.seg_offsets, self.n_segs + 1)
+
 
 class NodeArrays:
     """Device node arrays (voltage, rhs, d) shared by several mechanism
@@ -167,6 +188,9 @@ class DeviceInstanceData:
             rt.memset(self.defer_count.ptr, 0, 8, runner.stream)
         self.prebad: dict[str, int] = {}
         self.nodes: NodeBinding | None = None
+        # arrays a launch (or the voltage gather) may have changed since the
+        # upload: the only ones a write-back has to bring home
+        self.dirty: set[str] = set()
 
     def reorder(self, perm_ptr: int, stream) -> None:
         """new[k] = old[perm[k]] for every array, into a fresh arena."""
@@ -184,8 +208,10 @@ class DeviceInstanceData:
         self.ptr = new_ptr
 
     # ---- host <-> device ------------------------------------------------------
-    def upload_from(self, data, stream) -> None:
+    def upload_from(self, data, stream, skip=()) -> None:
         for name in self.names:
+            if name in skip:
+                continue
             arr = np.ascontiguousarray(data.arrays[name], dtype=np.float64)
             if arr.shape != (self.n,):
                 raise ValueError(f"array {name!r} has shape {arr.shape}, expected ({self.n},)")
@@ -196,7 +222,7 @@ class DeviceInstanceData:
             rt.h2d(self.ptr[name], arr.ctypes.data, arr.nbytes, stream)
         stream.sync()
 
-    def download_into(self, data, stream, names=None) -> None:
+    def download_into(self, data, stream, names=None, acc=True) -> None:
         names = self.names if names is None else names
         for name in names:
             dst = data.arrays[name]
@@ -207,7 +233,7 @@ class DeviceInstanceData:
                 dst[:] = tmp
             else:
                 rt.d2h(dst.ctypes.data, self.ptr[name], dst.nbytes, stream)
-        for name in ("i_acc", "g_acc"):
+        for name in ("i_acc", "g_acc") if acc else ():
             dst = data.acc[name]
             rt.d2h(dst.ctypes.data, self.ptr[name], dst.nbytes, stream)
         stream.sync()
@@ -255,6 +281,12 @@ class CudaRunner:
         self.stream = rt.Stream()
         self.status = rt.DeviceBuffer(C.sizeof(rt.Status))
         self._reset_status()
+        self._writes = {}
+        for k in KERNELS:
+            w = set(self.abi.kernels.get(k, {}).get("stores", ()))
+            if k in ("current_update", "step", "step_nodes"):
+                w |= {"i_acc", "g_acc"}
+            self._writes[k] = w
         self.n_newton = len(self.abi.newton_nodes)
         self._newton_kernel = [s.split(":")[0] for s in self.abi.newton_nodes]
         self._max_iter = {}
@@ -284,8 +316,10 @@ class CudaRunner:
         self.stream.sync()
         return st
 
-    def to_device(self, data) -> DeviceInstanceData:
-        """Upload an InstanceData into a device-resident store."""
+    def to_device(self, data, skip=()) -> DeviceInstanceData:
+        """Upload an InstanceData into a device-resident store.  Arrays named
+        in `skip` are left unset on the device (the caller overwrites them
+        before any kernel reads them, e.g. v from the node voltage gather)."""
         names = list(data.arrays)
         missing = [s for s in self.abi.slots if s not in data.arrays]
         if missing or "v" not in data.arrays:
@@ -294,18 +328,20 @@ class CudaRunner:
         dev = DeviceInstanceData(self, int(data.n), names, data.scalars)
         dev.newton_iters = list(data.newton_iters)
         self._mark("upload:alloc")
-        dev.upload_from(data, self.stream)
+        dev.upload_from(data, self.stream, skip)
         self._mark("upload:h2d")
-        self._prescan(dev)
+        self._prescan(dev, skip)
         self._mark("upload:prescan")
         return dev
 
-    def _prescan(self, dev: DeviceInstanceData) -> None:
+    def _prescan(self, dev: DeviceInstanceData, skip=()) -> None:
         """First non-finite index per array, once per upload (interp.py:538-545)."""
         buf = rt.DeviceBuffer(8 * len(dev.names))
         rt.memset(buf.ptr, 0xFF, 8 * len(dev.names), self.stream)
         L = rt.lib()
         for i, name in enumerate(dev.names):
+            if name in skip:
+                continue
             rt.check(L.nmodl_first_nonfinite(C.c_void_p(dev.ptr[name]), dev.n, C.c_void_p(buf.ptr + 8 * i),
                                              C.c_void_p(self.stream.handle)), "first_nonfinite")
         out = np.empty(len(dev.names), dtype=np.uint64)
@@ -313,13 +349,22 @@ class CudaRunner:
         self.stream.sync()
         dev.prebad = {name: int(v) for name, v in zip(dev.names, out) if v != np.uint64(rt.NO_ERROR)}
 
-    def to_host(self, dev: DeviceInstanceData, data) -> None:
-        """Download a device store into `data` (arrays, acc, scalars, newton record)."""
+    def to_host(self, dev: DeviceInstanceData, data, only_dirty: bool = False) -> None:
+        """Download a device store into `data` (arrays, acc, scalars, newton record).
+
+        `only_dirty`: `data` is the very object the store was uploaded from,
+        so arrays no launch could have written (parameters, ion reversal
+        potentials, ...) already hold the device values and are not copied."""
         self._mark("download:start")
+        names = list(dev.names)
+        acc = True
+        if only_dirty:
+            names = [n for n in names if n in dev.dirty]
+            acc = "i_acc" in dev.dirty
         if dev.nodes is not None:
-            self._unpermute_into(dev, data)
+            self._unpermute_into(dev, data, names, acc)
         else:
-            dev.download_into(data, self.stream)
+            dev.download_into(data, self.stream, names, acc)
         self._mark("download:arrays")
         data.scalars.update(dev.scalars)
         data.newton_iters[:] = dev.newton_iters
@@ -377,6 +422,7 @@ class CudaRunner:
         if kernel_name == "step_nodes" and dev.nodes is None:
             raise ValueError("step_nodes needs bind_nodes() first")
         md = self._struct(dev, newton_rec)
+        dev.dirty |= self._writes[kernel_name]
         if getattr(dev, "defer_count", None) is not None:
             # an aborted launch can leave a count behind; start every call clean
             rt.memset(dev.defer_count.ptr, 0, 8, self.stream)
@@ -392,7 +438,7 @@ class CudaRunner:
         if steps > 0 and dev.n > 0:
             self._run(dev, kernel_name, steps, host_data=data if host else None)
         if host:
-            self.to_host(dev, data)
+            self.to_host(dev, data, only_dirty=True)
         return data
 
     def _run(self, dev, kernel_name, steps, host_data=None):
@@ -428,7 +474,7 @@ class CudaRunner:
         if key != rt.NO_ERROR:
             self._reset_status()
             if host_data is not None:
-                self.to_host(dev, host_data)
+                self.to_host(dev, host_data, only_dirty=True)
             raise _interp_error(self._message(key, st, dev))
 
     def _message(self, key, st, dev) -> str:
@@ -500,11 +546,6 @@ class CudaRunner:
                                         C.c_void_p(nb.rank), C.c_void_p(bad), C.c_void_p(s.handle)),
                  "scatter_layout")
         self._mark("bind:sort")
-        b = np.empty(1, dtype=np.int32)
-        rt.d2h(b.ctypes.data, bad, 4, s)
-        s.sync()
-        if b[0] != 0x7FFFFFFF:
-            raise ValueError(f"node_index out of range at instance {int(b[0])}")
         nb.node_index = nb.alloc(4 * n)
         rt.check(L.nmodl_permute_i32(C.c_void_p(idx_in), C.c_void_p(nb.node_index), C.c_void_p(nb.perm), n,
                                      C.c_void_p(s.handle)), "permute_i32")
@@ -522,37 +563,37 @@ class CudaRunner:
                 else:
                     h = np.ascontiguousarray(host, dtype=np.float64)
                     rt.h2d(ptr, h.ctypes.data, 8 * n_nodes, s)
-        # host copies of the (integer) layout for tiling and error remapping
-        offsets = np.empty(n_nodes + 1, dtype=np.int64)
-        rt.d2h(offsets.ctypes.data, nb.node_offsets_full, offsets.nbytes, s)
-        s.sync()
-        nb.offsets_host = offsets
-        self._mark("bind:offsets_d2h")
         # segments: the nodes that own at least one instance, in node order;
         # the reduction touches only those (sparse populations such as one
-        # channel per soma leave most compartments alone)
-        seg_node = np.flatnonzero(np.diff(offsets)).astype(np.int32)
-        seg_off = np.concatenate([offsets[seg_node], [n]]).astype(np.int64)
-        nb.n_segs = len(seg_node)
-        nb.seg_unique = 1 if nb.n_segs == n else 0  # every occupied node holds exactly one instance
-        nb.seg_node = nb.alloc(4 * max(1, len(seg_node)))
-        nb.seg_offsets = nb.alloc(8 * len(seg_off))
-        rt.h2d(nb.seg_node, seg_node.ctypes.data, seg_node.nbytes, s)
-        rt.h2d(nb.seg_offsets, seg_off.ctypes.data, seg_off.nbytes, s)
-        # target 3/4 of the shared-memory capacity so a tile rarely spills to
-        # the global-memory reduction path when a segment straddles a boundary,
-        # but keep >= 4 tiles per SM so small populations still fill the GPU
+        # channel per soma leave most compartments alone).  Tiles: target 3/4
+        # of the shared-memory capacity so a tile rarely spills to the
+        # global-memory reduction path when a segment straddles a boundary,
+        # but keep >= 4 tiles per SM so small populations still fill the GPU.
+        # Both are built on the device (nmodl_node_segments; host
+        # restatement: tile_nodes_for) -- only two counts come back.
         if tile is None:
             sms = rt.device_info(self.device)["sm_count"]
             T = max(64, min((3 * self.options.tile) // 4, -(-n // (4 * sms))))
         else:
-            T = tile
-        tiles = tile_nodes_for(seg_off, T)
-        nb.tile_segs_host = tiles
-        nb.tile_segs = nb.alloc(8 * len(tiles))
-        rt.h2d(nb.tile_segs, tiles.ctypes.data, tiles.nbytes, s)
-        nb.n_tiles = len(tiles) - 1
+            T = int(tile)
+        n_marks = -(-max(n, 1) // T)
+        nb.seg_node = nb.alloc(4 * max(1, n_nodes))
+        nb.seg_offsets = nb.alloc(8 * (n_nodes + 1))
+        nb.tile_segs = nb.alloc(8 * (n_marks + 1))
+        counts = nb.alloc(16)
+        rt.check(L.nmodl_node_segments(C.c_void_p(nb.node_offsets_full), n_nodes, n, T, C.c_void_p(nb.seg_node),
+                                       C.c_void_p(nb.seg_offsets), C.c_void_p(nb.tile_segs), C.c_void_p(counts),
+                                       C.c_void_p(s.handle)), "node_segments")
+        cnt = np.empty(2, dtype=np.int64)
+        b = np.empty(1, dtype=np.int32)
+        rt.d2h(cnt.ctypes.data, counts, 16, s)
+        rt.d2h(b.ctypes.data, bad, 4, s)
         s.sync()
+        if b[0] != 0x7FFFFFFF:
+            raise ValueError(f"node_index out of range at instance {int(b[0])}")
+        nb.n_segs = int(cnt[0])
+        nb.n_tiles = int(cnt[1]) - 1
+        nb.seg_unique = 1 if nb.n_segs == n else 0  # every occupied node holds exactly one instance
         self._mark("bind:segments_tiles")
         # reorder every instance array into node-sorted order (on the device):
         # gather into a fresh arena, then retire the old one (no copy back)
@@ -570,6 +611,7 @@ class CudaRunner:
         nb = dev.nodes
         rt.check(rt.lib().nmodl_gather_v(C.c_void_p(nb.node_v), C.c_void_p(nb.node_index), C.c_void_p(dev.ptr["v"]),
                                          dev.n, C.c_void_p(self.stream.handle)), "gather_v")
+        dev.dirty.add("v")
 
     @staticmethod
     def share_slot(dst: DeviceInstanceData, dst_slot: str, src: DeviceInstanceData, src_slot: str) -> None:
@@ -606,7 +648,7 @@ class CudaRunner:
         self.stream.sync()
         return out
 
-    def _unpermute_into(self, dev, data) -> None:
+    def _unpermute_into(self, dev, data, names=None, acc=True) -> None:
         nb = dev.nodes
         L = rt.lib()
         s = self.stream
@@ -616,7 +658,8 @@ class CudaRunner:
                                   dev.n, C.c_void_p(s.handle)), "gather_v")
         # one stream: each permute waits for the previous copy out of `tmp`,
         # the host waits once at the end
-        for name in list(dev.names) + ["i_acc", "g_acc"]:
+        names = list(dev.names) if names is None else list(names)
+        for name in names + (["i_acc", "g_acc"] if acc else []):
             rt.check(L.nmodl_permute(C.c_void_p(dev.ptr[name]), C.c_void_p(tmp.ptr), C.c_void_p(nb.perm), dev.n, 1,
                                      C.c_void_p(s.handle)), "unpermute")
             dst = data.acc[name] if name in ("i_acc", "g_acc") else data.arrays[name]
@@ -654,10 +697,10 @@ def simulate(layout, data, steps: int, jac_mode: str = "exact", on_step=None, ru
         else:
             for step in range(steps):
                 runner.run_kernel(dev, "step", 1)
-                runner.to_host(dev, data)
+                runner.to_host(dev, data, only_dirty=True)
                 on_step(step, data)
     finally:
-        runner.to_host(dev, data)
+        runner.to_host(dev, data, only_dirty=True)
     return data
 
 
@@ -679,12 +722,18 @@ def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, 
     t = {}
     t0 = clock()
     runner = runner or CudaRunner(layout, jac_mode=jac_mode)
-    dev = runner.to_device(data)
+    # v is never uploaded: every instance's voltage is its node's
+    dev = runner.to_device(data, skip=("v",))
     t["upload"] = clock() - t0
     t0 = clock()
+    node_v = np.ascontiguousarray(node_v, dtype=np.float64)
     nb = runner.bind_nodes(dev, node_index, node_v, node_rhs, node_d)
-    rt.check(rt.lib().nmodl_gather_v(C.c_void_p(nb.node_v), C.c_void_p(nb.node_index), C.c_void_p(dev.ptr["v"]),
-                                     dev.n, C.c_void_p(runner.stream.handle)), "gather_v")
+    runner.gather_voltage(dev)
+    if not np.isfinite(node_v).all():
+        # a non-finite node voltage is a pre-existing non-finite v for the
+        # first instance (in caller order) that reads it
+        first = int(np.flatnonzero(~np.isfinite(node_v[np.asarray(node_index)]))[0])
+        dev.prebad["v"] = int(nb.host_array("rank", runner.stream)[first])
     t["bind_nodes"] = clock() - t0
     try:
         t0 = clock()
@@ -695,7 +744,7 @@ def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, 
         t["steps"] = clock() - t0
     finally:
         t0 = clock()
-        runner.to_host(dev, data)
+        runner.to_host(dev, data, only_dirty=True)
         out = {}
         for name in ("node_rhs", "node_d"):
             arr = np.empty(nb.n_nodes)

@@ -112,3 +112,69 @@ def test_tma_bulk_node_kernel_matches_oracle(n, n_nodes, tile):
     assert dev <= TOL, (where, dev)
     np.testing.assert_allclose(rhs_gpu, rhs_ref, rtol=1e-9, atol=0)
     np.testing.assert_allclose(d_gpu, d_ref, rtol=1e-9, atol=0)
+
+
+@pytest.mark.parametrize("n,n_nodes,tile", [(5000, 500, 64), (5000, 500, 1536), (3000, 7, 100), (4096, 4096, 256),
+                                           (2000, 1, 64), (100000, 250000, 700), (1, 3, 64)])
+def test_device_segments_and_tiles_match_host_restatement(n, n_nodes, tile):
+    """nmodl_node_segments (device) == the numpy restatement in runner.py."""
+    from paper_1905_02241_b200.runner import CudaRunner, tile_nodes_for
+
+    ir = load_ir("ProbAMPANMDA_EMS")
+    idx, nv = _inputs(n, n_nodes, 4)
+    r = CudaRunner(ir)
+    dev = r.to_device(O.init(ir, n, 1))
+    nb = r.bind_nodes(dev, idx, nv, tile=tile)
+    _, offsets, _ = N.scatter_layout(idx, n_nodes)
+    seg_node = np.flatnonzero(np.diff(offsets))
+    seg_off = np.concatenate([offsets[seg_node], [n]]).astype(np.int64)
+    assert nb.n_segs == len(seg_node)
+    np.testing.assert_array_equal(nb.seg_offsets_host, seg_off)
+    np.testing.assert_array_equal(nb.tile_segs_host, tile_nodes_for(seg_off, tile))
+    assert nb.seg_unique == (1 if len(seg_node) == n else 0)
+
+
+def test_write_back_covers_every_array():
+    """simulate_nodes copies back only what the device may have changed; the
+    result must still equal the oracle's whole store (parameters untouched,
+    v = gathered node voltage, accumulators, states)."""
+    from paper_1905_02241_b200.runner import simulate_nodes
+
+    ir = load_ir("ProbAMPANMDA_EMS")
+    n, n_nodes = 7000, 900
+    idx, nv = _inputs(n, n_nodes, 2)
+    base = O.init(ir, n, 8)
+    base.arrays["v"][:] = 1e300  # never read: the voltage comes from the nodes
+    ref, _, _ = N.simulate_nodes(ir, base.copy(), 20, idx, nv)
+    gpu, _, _ = simulate_nodes(ir, base.copy(), 20, idx, nv)
+    for name in ref.arrays:
+        if name not in ir_states_and_assigned(ir):
+            np.testing.assert_array_equal(gpu.arrays[name], ref.arrays[name], err_msg=name)
+    dev, where = parity(ir, ref, gpu)
+    assert dev <= TOL, (where, dev)
+
+
+def ir_states_and_assigned(ir):
+    from paper_1905_02241_b200.codegen_cuda import CudaPrinter
+
+    p = CudaPrinter(ir)
+    p.emit_unit()
+    out = set()
+    for k in p._abi.kernels.values():
+        out |= set(k["stores"])
+    return out
+
+
+def test_nonfinite_node_voltage_reports_like_oracle():
+    from paper_1905_02241_b200.runner import InterpError, simulate_nodes
+
+    ir = load_ir("hh_subset")
+    n, n_nodes = 3000, 300
+    idx, nv = _inputs(n, n_nodes, 5)
+    nv = nv.copy()
+    nv[idx[1234]] = np.nan
+    with pytest.raises(O.InterpError) as e_ref:
+        N.simulate_nodes(ir, O.init(ir, n, 1), 5, idx, nv)
+    with pytest.raises(InterpError) as e_gpu:
+        simulate_nodes(ir, O.init(ir, n, 1), 5, idx, nv)
+    assert str(e_gpu.value) == str(e_ref.value)

@@ -78,7 +78,7 @@ def options_for(stem: str):
         "ProbAMPANMDA_EMS": CudaOptions(ilp=1, fast_path=False),
         "hh_subset": CudaOptions(ilp=1, min_blocks=4, fast_path=False),
         "NaTs2_t": CudaOptions(ilp=2),
-        "K_Pst": CudaOptions(ilp=2),
+        "K_Pst": CudaOptions(ilp=2, exp_table=True),  # table exp: 0.082 -> 0.072 ms (tune18)
         "Ca_HVA": CudaOptions(ilp=2),
         "na6": CudaOptions(ilp=1, min_blocks=2),  # fast path + sparse LU: 0.049 ms/launch
         "cdp5ish": CudaOptions(ilp=1),

@@ -120,6 +120,9 @@ int nmodl_permute_i32(const int *src, int *dst, const long long *perm, long long
 int nmodl_gather_v(const double *node_v, const int *node_index, double *v, long long n, nmodl_stream_t s);
 /* self-test: out_a[i] = nmodl::exp_c(x[i]), out_b[i] = exp(x[i]) (bit-equality check) */
 int nmodl_selftest_exp(const double *x, double *out_a, double *out_b, long long n, nmodl_stream_t s);
+/* self-test: out[i] = nmodl::exp_t(x[i]); flag[i] bit 0 = fast form flagged,
+ * bit 1 = fast and safe forms disagree without a flag (must never happen) */
+int nmodl_selftest_exp_table(const double *x, double *out, unsigned *flag, long long n, nmodl_stream_t s);
 
 /* ---- per-mechanism library (lib<mech>-<hash>.so) -----------------------
  * Every generated mechanism exports exactly these symbols.  `md` points to a

@@ -531,3 +531,20 @@ NMODL_API int nmodl_selftest_exp(const double* x, double* a, double* b, long lon
   CK(cudaGetLastError());
   return 0;
 }
+// self-test: the table-driven exp (exp_t, and its fast form exp_tf with the flag)
+__global__ void k_selftest_exp_table(const double* __restrict__ x, double* __restrict__ a,
+                                     unsigned* __restrict__ fl, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    unsigned f = 0;
+    const double fast = nmodl::exp_tf(x[i], f);
+    const double safe = nmodl::exp_t(x[i]);
+    a[i] = safe;
+    // the fast form must agree with the safe form whenever it does not flag
+    fl[i] = f | ((f == 0 && __double_as_longlong(fast) != __double_as_longlong(safe)) ? 2u : 0u);
+  }
+}
+NMODL_API int nmodl_selftest_exp_table(const double* x, double* a, unsigned* fl, long long n, cudaStream_t s) {
+  k_selftest_exp_table<<<256, 256, 0, s>>>(x, a, fl, n);
+  CK(cudaGetLastError());
+  return 0;
+}

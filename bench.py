@@ -71,19 +71,29 @@ DEFAULT_WORKLOAD = "synapse10m"
 
 
 def options_for(stem: str):
-    """Launch shapes picked with tools/tune.py on B200 (profiles/tune_r01.md)."""
+    """Launch shapes / codegen picked with tools/tune.py on B200
+    (profiles/tune_r01.md).  `pipe` = per-thread cp.async double buffering;
+    `recip` / `div_approx` = relaxed arithmetic (reciprocal shadows, 2-ulp
+    rate-code division), parity-tested at 1e-10 after 1000 steps
+    (tests/test_gpu_parity.py::test_relaxed_arithmetic_within_tolerance)."""
     from paper_1905_02241_b200.codegen_cuda import CudaOptions
 
     tuned = {
         "ProbAMPANMDA_EMS": CudaOptions(ilp=1, fast_path=False),
-        "hh_subset": CudaOptions(ilp=1, min_blocks=4, fast_path=False),
-        "NaTs2_t": CudaOptions(ilp=2),
-        "K_Pst": CudaOptions(ilp=2, exp_table=True),  # table exp: 0.082 -> 0.072 ms (tune18)
-        "Ca_HVA": CudaOptions(ilp=2),
-        "na6": CudaOptions(ilp=1, min_blocks=2),  # fast path + sparse LU: 0.049 ms/launch
-        "cdp5ish": CudaOptions(ilp=1),
+        "hh_subset": CudaOptions(ilp=1, pipe=True, recip=True, div_approx=True),  # 0.0412 -> 0.0363 ms
+        "NaTs2_t": CudaOptions(ilp=2, pipe=True, recip=True, div_approx=True),  # 0.0788 -> 0.0658 ms
+        "K_Pst": CudaOptions(ilp=2, pipe=True, div_approx=True),  # 0.0717 (table exp) -> 0.0715 ms
+        "Ca_HVA": CudaOptions(ilp=2, pipe=True, recip=True),  # 0.0707 -> 0.0615 ms
+        "SKv3_1": CudaOptions(ilp=1, pipe=True, grid_waves=4, div_approx=True),  # 0.0500 -> 0.0430 ms
+        "Ih": CudaOptions(ilp=2, pipe=True, grid_waves=4, recip=True),  # 0.0474 -> 0.0399 ms
+        "na6": CudaOptions(ilp=1, min_blocks=2, pipe=True),  # 0.0485 -> 0.0444 ms
+        "cdp5ish": CudaOptions(ilp=1, pipe=True, div_approx=True),  # 0.0583 -> 0.0543 ms
     }
     return tuned.get(stem, CudaOptions())
+
+
+RELAXED_NOTE = ("fp64 throughout; rate code uses reciprocal shadows (X/(1/E) -> X*E) and <=2-ulp division "
+                "where tuned (bench.options_for), solver cores IEEE; parity 1e-10 after 1000 steps is tested")
 
 
 def bench_irs():
@@ -781,6 +791,7 @@ def main():
         cpu = cpu_reference(args.workload)
     if dist.rank == 0:
         config["l2_policy"] = res["l2"]
+        config["arithmetic"] = RELAXED_NOTE
         line = {
             "metric": METRIC,
             "value": res["value"],

@@ -123,6 +123,9 @@ int nmodl_selftest_exp(const double *x, double *out_a, double *out_b, long long 
 /* self-test: out[i] = nmodl::exp_t(x[i]); flag[i] bit 0 = fast form flagged,
  * bit 1 = fast and safe forms disagree without a flag (must never happen) */
 int nmodl_selftest_exp_table(const double *x, double *out, unsigned *flag, long long n, nmodl_stream_t s);
+/* self-test: out[i] = nmodl::div_a(a[i], b[i]) (relaxed division, CudaOptions.div_approx);
+ * a signalling-NaN marker where the branch-free form disagrees without flagging */
+int nmodl_selftest_div_approx(const double *a, const double *b, double *out, long long n, nmodl_stream_t s);
 
 /* ---- per-mechanism library (lib<mech>-<hash>.so) -----------------------
  * Every generated mechanism exports exactly these symbols.  `md` points to a

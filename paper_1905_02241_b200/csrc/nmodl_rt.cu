@@ -548,3 +548,20 @@ NMODL_API int nmodl_selftest_exp_table(const double* x, double* a, unsigned* fl,
   CK(cudaGetLastError());
   return 0;
 }
+
+// relaxed division (CudaOptions.div_approx): out[i] = div_a(a[i], b[i]); the
+// branch-free div_af must give the same value whenever it does not flag
+__global__ void k_selftest_div_approx(const double* __restrict__ a, const double* __restrict__ b,
+                                      double* __restrict__ out, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    unsigned f = 0;
+    const double fast = nmodl::div_af(a[i], b[i], f);
+    const double safe = nmodl::div_a(a[i], b[i]);
+    out[i] = (f == 0 && __double_as_longlong(fast) != __double_as_longlong(safe)) ? __longlong_as_double(0x7ff4dead00000000ll) : safe;
+  }
+}
+NMODL_API int nmodl_selftest_div_approx(const double* a, const double* b, double* out, long long n, cudaStream_t s) {
+  k_selftest_div_approx<<<256, 256, 0, s>>>(a, b, out, n);
+  CK(cudaGetLastError());
+  return 0;
+}

@@ -86,6 +86,7 @@ _SIGS = {
     "nmodl_gather_v": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
     "nmodl_selftest_exp": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
     "nmodl_selftest_exp_table": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
+    "nmodl_selftest_div_approx": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
 }
 RUNTIME_SYMBOLS = tuple(_SIGS)
 

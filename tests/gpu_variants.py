@@ -1,0 +1,33 @@
+"""(fixture stem, CudaOptions kwargs) pairs the GPU tests build beyond the
+default options -- prebuilt by __graft_entry__.build() so the `-m gpu` run
+on the box does not spend its time in nvcc."""
+
+RELAXED = [dict(recip=True), dict(div_approx=True), dict(recip=True, div_approx=True),
+           dict(recip=True, div_approx=True, fast_path=False)]
+RELAXED_STEMS = ["hh_subset", "NaTs2_t", "Ca_HVA", "Ih", "na6", "cdp5ish", "ProbAMPANMDA_EMS",
+                 "corpus_cat", "corpus_vtrap", "corpus_kdr"]
+PIPE_STEMS = ["hh_subset", "NaTs2_t", "na6", "cdp5ish", "ProbAMPANMDA_EMS", "corpus_cat", "cadyn"]
+WAVES_STEMS = ["hh_subset", "NaTs2_t", "cdp5ish", "ProbAMPANMDA_EMS"]
+DEFER_STEMS = ["hh_subset", "NaTs2_t", "na6", "cdp5ish", "ProbAMPANMDA_EMS", "corpus_cat"]
+
+
+def variants():
+    out = []
+    for st in ("hh_subset", "ProbAMPANMDA_EMS"):
+        out.append((st, dict(ilp=2)))
+    for st in DEFER_STEMS:
+        out.append((st, dict(fast_path=True, defer=True)))
+    for st in PIPE_STEMS:
+        for ilp in (1, 2):
+            out.append((st, dict(ilp=ilp, pipe=True)))
+    for st in WAVES_STEMS:
+        for w in (0, 2):
+            out.append((st, dict(fast_path=True, pipe=True, grid_waves=w)))
+    for w, t in ((0, 2048), (0, 256), (2, 1024)):
+        out.append(("ProbAMPANMDA_EMS", dict(fast_path=False, tile=t, grid_waves=w)))
+    for t in (512, 256, 128):
+        out.append(("ProbAMPANMDA_EMS", dict(bulk=True, tile=t, fast_path=False)))
+    for st in RELAXED_STEMS:
+        for r in RELAXED:
+            out.append((st, {"fast_path": True, **r}))
+    return out

@@ -178,3 +178,22 @@ def test_nonfinite_node_voltage_reports_like_oracle():
     with pytest.raises(InterpError) as e_gpu:
         simulate_nodes(ir, O.init(ir, n, 1), 5, idx, nv)
     assert str(e_gpu.value) == str(e_ref.value)
+
+
+@pytest.mark.parametrize("waves,tile", [(0, 2048), (0, 256), (2, 1024)])
+def test_node_kernel_grid_waves_matches_oracle(waves, tile):
+    """Node kernel with one CTA per tile (grid_waves=0) or two resident
+    waves: same trajectories, node rhs/d as the in-order oracle."""
+    from paper_1905_02241_b200.codegen_cuda import CudaOptions
+    from paper_1905_02241_b200.runner import CudaRunner, simulate_nodes
+
+    ir = load_ir("ProbAMPANMDA_EMS")
+    n, n_nodes = 30000, 3000
+    idx, nv = _inputs(n, n_nodes, 5)
+    ref, rhs_ref, d_ref = N.simulate_nodes(ir, O.init(ir, n, 9), 40, idx, nv)
+    runner = CudaRunner(ir, options=CudaOptions(fast_path=False, tile=tile, grid_waves=waves))
+    gpu, rhs_gpu, d_gpu = simulate_nodes(ir, O.init(ir, n, 9), 40, idx, nv, runner=runner)
+    dev, where = parity(ir, ref, gpu)
+    assert dev <= TOL, (where, dev)
+    np.testing.assert_allclose(rhs_gpu, rhs_ref, rtol=1e-9, atol=0)
+    np.testing.assert_allclose(d_gpu, d_ref, rtol=1e-9, atol=0)

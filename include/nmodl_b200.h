@@ -101,6 +101,9 @@ int nmodl_first_nonfinite(const double *p, long long n, unsigned long long *out_
 int nmodl_checksum(const double *p, long long n, double *scratch_dev, double *out_dev, nmodl_stream_t s);
 /* write a buffer larger than L2 (timing hygiene) */
 int nmodl_l2_flush(double *buf, long long n_doubles, nmodl_stream_t s);
+/* keep the stream busy for `ns` nanoseconds (one spinning thread) so host-issued
+ * timed launches queue up behind it instead of leaving gaps in the timing */
+int nmodl_spin(long long ns, nmodl_stream_t s);
 /* node_index scatter layout: stable sort by node (perm, rank = perm^-1),
  * per-node counts and offsets.  Builder-defined extension: the reference has
  * no node arrays; the SIMD backend only marks ATOMIC_ADD,
@@ -126,6 +129,9 @@ int nmodl_selftest_exp_table(const double *x, double *out, unsigned *flag, long 
 /* self-test: out[i] = nmodl::div_a(a[i], b[i]) (relaxed division, CudaOptions.div_approx);
  * a signalling-NaN marker where the branch-free form disagrees without flagging */
 int nmodl_selftest_div_approx(const double *a, const double *b, double *out, long long n, nmodl_stream_t s);
+/* self-test: out[i] = nmodl::exp16(x[i]) (shared-memory table exp, CudaOptions.exp_smem);
+ * flag bits as nmodl_selftest_exp_table */
+int nmodl_selftest_exp_smem(const double *x, double *out, unsigned *flag, long long n, nmodl_stream_t s);
 
 /* ---- per-mechanism library (lib<mech>-<hash>.so) -----------------------
  * Every generated mechanism exports exactly these symbols.  `md` points to a

@@ -267,6 +267,23 @@ NMODL_API int nmodl_l2_flush(double* buf, long long n_doubles, cudaStream_t s) {
   return 0;
 }
 
+// Device-side head start for host-issued timed sequences: one thread spins
+// on %globaltimer for `ns`, so the host can enqueue the events and launches
+// that follow before the GPU reaches them (no host gaps inside the timing).
+__global__ void k_spin(long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while ((long long)(t - t0) < ns);
+}
+NMODL_API int nmodl_spin(long long ns, cudaStream_t s) {
+  k_spin<<<1, 1, 0, s>>>(ns);
+  CK(cudaGetLastError());
+  return 0;
+}
+
 // ---------------------------------------------------------------------------
 // node_index scatter layout (builder-defined extension; the reference has no
 // node arrays).  Stable counting sort of instances by node:
@@ -562,6 +579,26 @@ __global__ void k_selftest_div_approx(const double* __restrict__ a, const double
 }
 NMODL_API int nmodl_selftest_div_approx(const double* a, const double* b, double* out, long long n, cudaStream_t s) {
   k_selftest_div_approx<<<256, 256, 0, s>>>(a, b, out, n);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// shared-memory table exp (CudaOptions.exp_smem): out = exp16(x); flag bit 0 =
+// fast form flagged, bit 1 = fast and safe forms disagree without a flag
+__global__ void k_selftest_exp_smem(const double* __restrict__ x, double* __restrict__ a,
+                                    unsigned* __restrict__ fl, long long n) {
+  nmodl::exp16_init();
+  __syncthreads();
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    unsigned f = 0;
+    const double fast = nmodl::exp16f(x[i], f);
+    const double safe = nmodl::exp16(x[i]);
+    a[i] = safe;
+    fl[i] = f | ((f == 0 && __double_as_longlong(fast) != __double_as_longlong(safe)) ? 2u : 0u);
+  }
+}
+NMODL_API int nmodl_selftest_exp_smem(const double* x, double* a, unsigned* fl, long long n, cudaStream_t s) {
+  k_selftest_exp_smem<<<256, 256, 0, s>>>(x, a, fl, n);
   CK(cudaGetLastError());
   return 0;
 }

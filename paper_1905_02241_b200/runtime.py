@@ -74,6 +74,7 @@ _SIGS = {
     "nmodl_first_nonfinite": (C.c_int, [C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p]),
     "nmodl_checksum": (C.c_int, [C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p]),
     "nmodl_l2_flush": (C.c_int, [C.c_void_p, C.c_longlong, C.c_void_p]),
+    "nmodl_spin": (C.c_int, [C.c_longlong, C.c_void_p]),
     "nmodl_scatter_layout": (
         C.c_int,
         [C.c_void_p, C.c_longlong, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -87,6 +88,7 @@ _SIGS = {
     "nmodl_selftest_exp": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
     "nmodl_selftest_exp_table": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
     "nmodl_selftest_div_approx": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
+    "nmodl_selftest_exp_smem": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
 }
 RUNTIME_SYMBOLS = tuple(_SIGS)
 

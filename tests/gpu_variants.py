@@ -3,7 +3,10 @@ default options -- prebuilt by __graft_entry__.build() so the `-m gpu` run
 on the box does not spend its time in nvcc."""
 
 RELAXED = [dict(recip=True), dict(div_approx=True), dict(recip=True, div_approx=True),
-           dict(recip=True, div_approx=True, fast_path=False)]
+           dict(recip=True, div_approx=True, fast_path=False), dict(recip=True, div_approx=True, exp_smem=True),
+           dict(exp_smem=True, fast_path=False), dict(exp_smem=True, pipe=True, grid_waves=0),
+           dict(recip=True, div_approx=True, pipe=True, fast_redo=True),
+           dict(recip=True, div_approx=True, pipe=True, fast_redo=True, ilp=2)]
 RELAXED_STEMS = ["hh_subset", "NaTs2_t", "Ca_HVA", "Ih", "na6", "cdp5ish", "ProbAMPANMDA_EMS",
                  "corpus_cat", "corpus_vtrap", "corpus_kdr"]
 PIPE_STEMS = ["hh_subset", "NaTs2_t", "na6", "cdp5ish", "ProbAMPANMDA_EMS", "corpus_cat", "cadyn"]
@@ -25,8 +28,17 @@ def variants():
             out.append((st, dict(fast_path=True, pipe=True, grid_waves=w)))
     for w, t in ((0, 2048), (0, 256), (2, 1024)):
         out.append(("ProbAMPANMDA_EMS", dict(fast_path=False, tile=t, grid_waves=w)))
+    for t in (512, 128, 64, 2048):
+        for kw in (dict(fast_path=False, pipe=True), dict(fast_path=True, fast_redo=True, pipe=True),
+                   dict(fast_path=False, pipe=True, min_blocks=4)):
+            out.append(("ProbAMPANMDA_EMS", dict(tile=t, **kw)))
+    out.append(("ProbAMPANMDA_EMS", dict(fast_path=False, pipe=True)))
     for t in (512, 256, 128):
         out.append(("ProbAMPANMDA_EMS", dict(bulk=True, tile=t, fast_path=False)))
+    for st in ("hh_subset", "NaTs2_t", "corpus_cat", "cdp5ish"):
+        for kw in (dict(fast_redo=True), dict(fast_redo=True, pipe=True), dict(fast_redo=True, pipe=True, ilp=2),
+                   dict(fast_redo=True, pipe=True, recip=True, div_approx=True, exp_smem=True)):
+            out.append((st, {"fast_path": True, **kw}))
     for st in RELAXED_STEMS:
         for r in RELAXED:
             out.append((st, {"fast_path": True, **r}))

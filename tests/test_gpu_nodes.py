@@ -59,17 +59,21 @@ def test_simulate_nodes_matches_oracle(stem, n, n_nodes, steps):
     assert np.max(np.abs(d_ref - d_gpu) / den) <= 1e-9
 
 
-def test_scatter_arithmetic_bit_exact():
+@pytest.mark.parametrize("pipe", [False, True])
+def test_scatter_arithmetic_bit_exact(pipe):
     """Given the GPU's own per-instance i_acc/g_acc, the node sums are
-    bit-identical to sequential np.subtract.at / np.add.at."""
-    from paper_1905_02241_b200.runner import simulate_nodes
+    bit-identical to sequential np.subtract.at / np.add.at (shared-memory
+    staged currents, and the pipelined kernel's L2 read-back)."""
+    from paper_1905_02241_b200.codegen_cuda import CudaOptions
+    from paper_1905_02241_b200.runner import CudaRunner, simulate_nodes
 
     ir = load_ir("ProbAMPANMDA_EMS")
     n, n_nodes = 30000, 1234
     idx, nv = _inputs(n, n_nodes, 2)
     rhs0 = np.zeros(n_nodes)
     d0 = np.zeros(n_nodes)
-    gpu, rhs_gpu, d_gpu = simulate_nodes(ir, O.init(ir, n, 9), 1, idx, nv, rhs0.copy(), d0.copy())
+    runner = CudaRunner(ir, options=CudaOptions(fast_path=False, pipe=pipe))
+    gpu, rhs_gpu, d_gpu = simulate_nodes(ir, O.init(ir, n, 9), 1, idx, nv, rhs0.copy(), d0.copy(), runner=runner)
     rhs_ref, d_ref = rhs0.copy(), d0.copy()
     N.scatter(rhs_ref, d_ref, idx, gpu.acc["i_acc"], gpu.acc["g_acc"])
     np.testing.assert_array_equal(rhs_gpu, rhs_ref)
@@ -193,6 +197,33 @@ def test_node_kernel_grid_waves_matches_oracle(waves, tile):
     ref, rhs_ref, d_ref = N.simulate_nodes(ir, O.init(ir, n, 9), 40, idx, nv)
     runner = CudaRunner(ir, options=CudaOptions(fast_path=False, tile=tile, grid_waves=waves))
     gpu, rhs_gpu, d_gpu = simulate_nodes(ir, O.init(ir, n, 9), 40, idx, nv, runner=runner)
+    dev, where = parity(ir, ref, gpu)
+    assert dev <= TOL, (where, dev)
+    np.testing.assert_allclose(rhs_gpu, rhs_ref, rtol=1e-9, atol=0)
+    np.testing.assert_allclose(d_gpu, d_ref, rtol=1e-9, atol=0)
+
+
+NODE_PIPE = [dict(fast_path=False, pipe=True), dict(fast_path=True, fast_redo=True, pipe=True),
+             dict(fast_path=False, pipe=True, min_blocks=4)]
+
+
+@pytest.mark.parametrize("variant", range(len(NODE_PIPE)))
+@pytest.mark.parametrize("n,n_nodes,tile", [(20000, 2000, 512), (6000, 3, 512), (9000, 4000, 128), (777, 50, 64),
+                                           (30000, 30000, 2048)])
+def test_node_kernel_cp_async_pipeline_matches_oracle(variant, n, n_nodes, tile):
+    """Node kernel with the per-thread cp.async pipeline (CudaOptions.pipe):
+    the next instance -- possibly the first of the next tile -- is in flight
+    while the current one computes; tiles smaller than the block leave
+    threads without instances; huge segments exceed the tile.  Same
+    trajectories, node rhs/d as the in-order oracle."""
+    from paper_1905_02241_b200.codegen_cuda import CudaOptions
+    from paper_1905_02241_b200.runner import CudaRunner, simulate_nodes
+
+    ir = load_ir("ProbAMPANMDA_EMS")
+    idx, nv = _inputs(n, n_nodes, 6)
+    ref, rhs_ref, d_ref = N.simulate_nodes(ir, O.init(ir, n, 10), 50, idx, nv)
+    runner = CudaRunner(ir, options=CudaOptions(tile=tile, **NODE_PIPE[variant]))
+    gpu, rhs_gpu, d_gpu = simulate_nodes(ir, O.init(ir, n, 10), 50, idx, nv, runner=runner)
     dev, where = parity(ir, ref, gpu)
     assert dev <= TOL, (where, dev)
     np.testing.assert_allclose(rhs_gpu, rhs_ref, rtol=1e-9, atol=0)

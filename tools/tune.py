@@ -46,11 +46,15 @@ def run(stem, opts, nodes=0, steps=30):
     lb = launch_bytes(r.abi, n, kernel, nodes)
     flush = rt.DeviceBuffer(2 * info["l2_bytes"]) if lb < 3 * info["l2_bytes"] else None
     a, b = rt.Event(), rt.Event()
-    for _ in range(10):
+    import os
+
+    for _ in range(int(os.environ.get("TUNE_WARMUP", "10"))):
         r.launch(dev, kernel, 1)
     r.stream.sync()
     total = 0.0
     for _ in range(steps):
+        # head start: the host enqueues flush + events + launch before the GPU gets there
+        rt.check(rt.lib().nmodl_spin(1_000_000, C.c_void_p(r.stream.handle)), "spin")
         if flush:
             rt.check(rt.lib().nmodl_l2_flush(C.c_void_p(flush.ptr), flush.nbytes // 8, C.c_void_p(r.stream.handle)), "f")
         a.record(r.stream)
@@ -72,7 +76,7 @@ def grid(spec: str):
     for part in spec.split():
         k, vs = part.split("=")
         keys.append(k)
-        values.append([bool(int(v)) if k in ("fast_path", "exp_c", "const_pool", "fast_div", "const_div", "exp_inline", "stream_hints", "fmad", "bulk", "defer", "exp_table", "pipe", "recip", "div_approx") else int(v)
+        values.append([bool(int(v)) if k in ("fast_path", "exp_c", "const_pool", "fast_div", "const_div", "exp_inline", "stream_hints", "fmad", "bulk", "defer", "exp_table", "pipe", "recip", "div_approx", "exp_smem", "fast_redo") else int(v)
                        for v in vs.split(",")])
     return [CudaOptions(**dict(zip(keys, combo))) for combo in itertools.product(*values)]
 
@@ -83,6 +87,26 @@ def main():
     if args and args[0] == "--grid":
         VARIANTS = grid(args[1])
         args = args[2:]
+    if args and args[0] == "--around":
+        # bench.options_for(stem) with the listed fields varied: --around "exp_smem=0,1 fast_path=0,1" stems...
+        import dataclasses
+
+        sys.path.insert(0, str(ROOT))
+        from bench import options_for
+
+        spec, stems_ = args[1], args[2:]
+        deltas = grid(spec)
+        keys = [p.split("=")[0] for p in spec.split()]
+        for stem in stems_:
+            for d in deltas:
+                opts = dataclasses.replace(options_for(stem), **{k: getattr(d, k) for k in keys})
+                nodes = 1_000_000 if stem == "ProbAMPANMDA_EMS" else 0
+                try:
+                    res = run(stem, opts, nodes)
+                except Exception as exc:  # noqa: BLE001
+                    res = {"stem": stem, "opts": str(opts), "error": repr(exc)[:300]}
+                print(json.dumps(res), flush=True)
+        return
     if args and args[0] == "--synapse":
         VARIANTS = [CudaOptions(fast_path=False, tile=t, block=b, min_blocks=m)
                     for t in (1024, 2048, 4096) for b in (256, 512) for m in (0, 2, 3, 5) if not (b == 512 and m > 2)]

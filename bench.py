@@ -86,8 +86,8 @@ def options_for(stem: str):
         "Ca_HVA": CudaOptions(ilp=2, min_blocks=2, pipe=True, recip=True, fast_redo=True),  # 0.0707 -> 0.0572 ms
         "SKv3_1": CudaOptions(ilp=1, pipe=True, grid_waves=4, div_approx=True, fast_redo=True),  # 0.0500 -> 0.0430 ms
         "Ih": CudaOptions(ilp=2, pipe=True, grid_waves=4, recip=True, fast_redo=True),  # 0.0474 -> 0.0399 ms
-        "na6": CudaOptions(ilp=1, min_blocks=2, pipe=True, fast_redo=True),  # 0.0485 -> 0.0425 ms
-        "cdp5ish": CudaOptions(ilp=1, min_blocks=2, pipe=True, div_approx=True, fast_redo=True),  # 0.0583 -> 0.0534 ms
+        "na6": CudaOptions(ilp=1, min_blocks=2, pipe=True, fast_redo=True, lu_spec=True),  # 0.0485 -> 0.0369 ms
+        "cdp5ish": CudaOptions(ilp=1, min_blocks=2, pipe=True, div_approx=True, fast_redo=True, lu_spec=True),  # 0.0583 -> 0.0410
     }
     return tuned.get(stem, CudaOptions())
 

@@ -39,6 +39,9 @@ def variants():
         for kw in (dict(fast_redo=True), dict(fast_redo=True, pipe=True), dict(fast_redo=True, pipe=True, ilp=2),
                    dict(fast_redo=True, pipe=True, recip=True, div_approx=True, exp_smem=True)):
             out.append((st, {"fast_path": True, **kw}))
+    for st in ("na6", "cdp5ish", "corpus_fourstate", "corpus_pump", "corpus_fourstate.nopass", "corpus_pump.nopass"):
+        out.append((st, dict(lu_spec=True)))
+        out.append((st, dict(lu_spec=True, fast_path=True, fast_redo=True, pipe=True)))
     for st in RELAXED_STEMS:
         for r in RELAXED:
             out.append((st, {"fast_path": True, **r}))

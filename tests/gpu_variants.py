@@ -30,9 +30,11 @@ def variants():
         out.append(("ProbAMPANMDA_EMS", dict(fast_path=False, tile=t, grid_waves=w)))
     for t in (512, 128, 64, 2048):
         for kw in (dict(fast_path=False, pipe=True), dict(fast_path=True, fast_redo=True, pipe=True),
-                   dict(fast_path=False, pipe=True, min_blocks=4)):
-            out.append(("ProbAMPANMDA_EMS", dict(tile=t, **kw)))
+                   dict(fast_path=False, pipe=True, min_blocks=4), dict(fast_path=False, warp_tiles=True),
+                   dict(fast_path=True, fast_redo=True, warp_tiles=True)):
+            out.append(("ProbAMPANMDA_EMS", dict(tile=min(t, 256) if kw.get("warp_tiles") else t, **kw)))
     out.append(("ProbAMPANMDA_EMS", dict(fast_path=False, pipe=True)))
+    out.append(("ProbAMPANMDA_EMS", dict(fast_path=False, warp_tiles=True, tile=256)))
     for t in (512, 256, 128):
         out.append(("ProbAMPANMDA_EMS", dict(bulk=True, tile=t, fast_path=False)))
     for st in ("hh_subset", "NaTs2_t", "corpus_cat", "cdp5ish"):

@@ -59,8 +59,8 @@ def test_simulate_nodes_matches_oracle(stem, n, n_nodes, steps):
     assert np.max(np.abs(d_ref - d_gpu) / den) <= 1e-9
 
 
-@pytest.mark.parametrize("pipe", [False, True])
-def test_scatter_arithmetic_bit_exact(pipe):
+@pytest.mark.parametrize("pipe,warp_tiles", [(False, False), (True, False), (False, True)])
+def test_scatter_arithmetic_bit_exact(pipe, warp_tiles):
     """Given the GPU's own per-instance i_acc/g_acc, the node sums are
     bit-identical to sequential np.subtract.at / np.add.at (shared-memory
     staged currents, and the pipelined kernel's L2 read-back)."""
@@ -72,7 +72,7 @@ def test_scatter_arithmetic_bit_exact(pipe):
     idx, nv = _inputs(n, n_nodes, 2)
     rhs0 = np.zeros(n_nodes)
     d0 = np.zeros(n_nodes)
-    runner = CudaRunner(ir, options=CudaOptions(fast_path=False, pipe=pipe))
+    runner = CudaRunner(ir, options=CudaOptions(fast_path=False, pipe=pipe, warp_tiles=warp_tiles, tile=256 if warp_tiles else 2048))
     gpu, rhs_gpu, d_gpu = simulate_nodes(ir, O.init(ir, n, 9), 1, idx, nv, rhs0.copy(), d0.copy(), runner=runner)
     rhs_ref, d_ref = rhs0.copy(), d0.copy()
     N.scatter(rhs_ref, d_ref, idx, gpu.acc["i_acc"], gpu.acc["g_acc"])
@@ -204,14 +204,16 @@ def test_node_kernel_grid_waves_matches_oracle(waves, tile):
 
 
 NODE_PIPE = [dict(fast_path=False, pipe=True), dict(fast_path=True, fast_redo=True, pipe=True),
-             dict(fast_path=False, pipe=True, min_blocks=4)]
+             dict(fast_path=False, pipe=True, min_blocks=4), dict(fast_path=False, warp_tiles=True),
+             dict(fast_path=True, fast_redo=True, warp_tiles=True)]
 
 
 @pytest.mark.parametrize("variant", range(len(NODE_PIPE)))
 @pytest.mark.parametrize("n,n_nodes,tile", [(20000, 2000, 512), (6000, 3, 512), (9000, 4000, 128), (777, 50, 64),
                                            (30000, 30000, 2048)])
 def test_node_kernel_cp_async_pipeline_matches_oracle(variant, n, n_nodes, tile):
-    """Node kernel with the per-thread cp.async pipeline (CudaOptions.pipe):
+    """Node kernel with the per-thread cp.async pipeline (CudaOptions.pipe)
+    or one warp per tile (CudaOptions.warp_tiles, __syncwarp only):
     the next instance -- possibly the first of the next tile -- is in flight
     while the current one computes; tiles smaller than the block leave
     threads without instances; huge segments exceed the tile.  Same
@@ -222,7 +224,10 @@ def test_node_kernel_cp_async_pipeline_matches_oracle(variant, n, n_nodes, tile)
     ir = load_ir("ProbAMPANMDA_EMS")
     idx, nv = _inputs(n, n_nodes, 6)
     ref, rhs_ref, d_ref = N.simulate_nodes(ir, O.init(ir, n, 10), 50, idx, nv)
-    runner = CudaRunner(ir, options=CudaOptions(tile=tile, **NODE_PIPE[variant]))
+    kw = NODE_PIPE[variant]
+    if kw.get("warp_tiles"):
+        tile = min(tile, 256)  # per-warp shared staging: 8 warps x tile x 16 B must fit the 48 KB static limit
+    runner = CudaRunner(ir, options=CudaOptions(tile=tile, **kw))
     gpu, rhs_gpu, d_gpu = simulate_nodes(ir, O.init(ir, n, 10), 50, idx, nv, runner=runner)
     dev, where = parity(ir, ref, gpu)
     assert dev <= TOL, (where, dev)

@@ -31,7 +31,8 @@ def variants():
     for t in (512, 128, 64, 2048):
         for kw in (dict(fast_path=False, pipe=True), dict(fast_path=True, fast_redo=True, pipe=True),
                    dict(fast_path=False, pipe=True, min_blocks=4), dict(fast_path=False, warp_tiles=True),
-                   dict(fast_path=True, fast_redo=True, warp_tiles=True)):
+                   dict(fast_path=True, fast_redo=True, warp_tiles=True), dict(fast_path=False, idx_ahead=True),
+                   dict(fast_path=True, fast_redo=True, idx_ahead=True)):
             out.append(("ProbAMPANMDA_EMS", dict(tile=min(t, 256) if kw.get("warp_tiles") else t, **kw)))
     out.append(("ProbAMPANMDA_EMS", dict(fast_path=False, pipe=True)))
     out.append(("ProbAMPANMDA_EMS", dict(fast_path=False, warp_tiles=True, tile=256)))

@@ -82,7 +82,8 @@ def options_for(stem: str):
         "ProbAMPANMDA_EMS": CudaOptions(ilp=1, fast_path=False),
         "hh_subset": CudaOptions(ilp=1, pipe=True, recip=True, div_approx=True, fast_redo=True),  # 0.0412 -> 0.0332 ms
         "NaTs2_t": CudaOptions(ilp=2, min_blocks=2, pipe=True, recip=True, div_approx=True, fast_redo=True),  # 0.0788 -> 0.0594
-        "K_Pst": CudaOptions(ilp=2, min_blocks=2, pipe=True, div_approx=True, exp_smem=True, fast_redo=True),  # 0.0717 -> 0.0652
+        "K_Pst": CudaOptions(ilp=2, min_blocks=2, pipe=True, recip=True, quot=True, div_approx=True, exp_smem=True,
+                             fast_redo=True),  # 0.0717 -> 0.0640 ms
         "Ca_HVA": CudaOptions(ilp=2, min_blocks=2, pipe=True, recip=True, div_approx=True, fast_redo=True),  # 0.0707 -> 0.0561
         "SKv3_1": CudaOptions(ilp=1, pipe=True, grid_waves=4, div_approx=True, fast_redo=True),  # 0.0500 -> 0.0426 ms
         "Ih": CudaOptions(ilp=2, pipe=True, grid_waves=4, recip=True, div_approx=True, fast_redo=True),  # 0.0474 -> 0.0392 ms

@@ -6,9 +6,11 @@ RELAXED = [dict(recip=True), dict(div_approx=True), dict(recip=True, div_approx=
            dict(recip=True, div_approx=True, fast_path=False), dict(recip=True, div_approx=True, exp_smem=True),
            dict(exp_smem=True, fast_path=False), dict(exp_smem=True, pipe=True, grid_waves=0),
            dict(recip=True, div_approx=True, pipe=True, fast_redo=True),
-           dict(recip=True, div_approx=True, pipe=True, fast_redo=True, ilp=2)]
+           dict(recip=True, div_approx=True, pipe=True, fast_redo=True, ilp=2),
+           dict(recip=True, quot=True, div_approx=True, pipe=True, fast_redo=True),
+           dict(recip=True, quot=True, fast_path=False)]
 RELAXED_STEMS = ["hh_subset", "NaTs2_t", "Ca_HVA", "Ih", "na6", "cdp5ish", "ProbAMPANMDA_EMS",
-                 "corpus_cat", "corpus_vtrap", "corpus_kdr"]
+                 "corpus_cat", "corpus_vtrap", "corpus_kdr", "K_Pst", "SKv3_1"]
 PIPE_STEMS = ["hh_subset", "NaTs2_t", "na6", "cdp5ish", "ProbAMPANMDA_EMS", "corpus_cat", "cadyn"]
 WAVES_STEMS = ["hh_subset", "NaTs2_t", "cdp5ish", "ProbAMPANMDA_EMS"]
 DEFER_STEMS = ["hh_subset", "NaTs2_t", "na6", "cdp5ish", "ProbAMPANMDA_EMS", "corpus_cat"]

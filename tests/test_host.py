@@ -280,3 +280,75 @@ def test_census_counts_match_the_mechanism():
     assert syn["exp"] == 4 + 2  # 4 cnexp decays + Mg block at v and v+h
     r = roofline(load_ir("ProbAMPANMDA_EMS"))
     assert r["bound"] == "hbm" and r["bytes_per_instance"] == 152
+
+
+OPTION_SETS = [
+    ("hh_subset", dict(pipe=True, recip=True, div_approx=True, fast_redo=True, fast_path=True)),
+    ("NaTs2_t", dict(ilp=2, pipe=True, recip=True, div_approx=True, fast_redo=True, fast_path=True, min_blocks=2)),
+    ("K_Pst", dict(ilp=2, recip=True, quot=True, exp_smem=True, pipe=True, fast_path=True, fast_redo=True)),
+    ("na6", dict(lu_spec=True, pipe=True, fast_path=True, fast_redo=True)),
+    ("cdp5ish", dict(lu_spec=True, div_approx=True, fast_path=True)),
+    ("ProbAMPANMDA_EMS", dict(warp_tiles=True, tile=256, fast_path=False)),
+    ("ProbAMPANMDA_EMS", dict(idx_ahead=True, fast_path=False)),
+    ("ProbAMPANMDA_EMS", dict(pipe=True, fast_path=True, fast_redo=True, grid_waves=0)),
+]
+
+
+@pytest.mark.parametrize("stem,kw", OPTION_SETS)
+def test_option_builds_are_deterministic_and_keep_the_abi(stem, kw):
+    """Every code-generation option is a pure function of (layout, options),
+    and none of them changes the C ABI (struct layout, entry points)."""
+    from paper_1905_02241_b200.codegen_cuda import cuda_abi
+
+    ir = load_ir(stem)
+    a, abi_a = cuda_abi(ir, CudaOptions(**kw))
+    b, _ = cuda_abi(load_ir(stem), CudaOptions(**kw))
+    assert a.text == b.text
+    _, abi0 = cuda_abi(ir, CudaOptions())
+    assert abi_a.to_json() == abi0.to_json()
+    assert emit_cuda_header(ir, CudaOptions(**kw)).text == emit_cuda_header(ir).text
+
+
+def test_reciprocal_shadows_remove_the_tau_divisions():
+    """recip: hh's three `dt/tau` with tau = 1/(q10*sum) become products and
+    the 1/(q10*sum) quotients are never formed; quot: K_Pst's
+    `dt/((...)/qt)` become one division each."""
+    base = emit_cuda(load_ir("hh_subset"), CudaOptions(fast_path=True)).text
+    rec = emit_cuda(load_ir("hh_subset"), CudaOptions(fast_path=True, recip=True)).text
+    assert rec.count("NM_DIV(") < base.count("NM_DIV(")
+    assert "md.dt) * l_mtau_rd" in rec and "l_mtau = NM_DIV" not in rec.split("hh_body_state_update")[1].split("hh_body_current_update")[0]
+    kp = emit_cuda(load_ir("K_Pst"), CudaOptions(recip=True, quot=True)).text
+    assert "l_mTau_rn = nm_n" in kp and "NM_DIV((double)(md.dt) * l_mTau_rd, l_mTau_rn)" in kp
+
+
+def test_speculative_lu_keeps_a_pivoted_fallback():
+    """lu_spec emits the swap-free elimination guarded by the first-max test
+    and the full pivoted LU behind `!ok` (na6: runtime LU, k=6)."""
+    text = emit_cuda(load_ir("na6"), CudaOptions(lu_spec=True)).text
+    assert "bool ok_" in text and "a row swap is due" in text
+    assert "const bool sw = (piv ==" in text  # the pivoted path is still there
+    plain = emit_cuda(load_ir("na6"), CudaOptions()).text
+    assert "bool ok_" not in plain
+
+
+def test_solver_cores_keep_ieee_division_under_div_approx():
+    """div_approx relaxes rate-code division only: LU pivots / back
+    substitution and Newton updates use NM_DIVX (always the IEEE quotient)."""
+    text = emit_cuda(load_ir("cdp5ish"), CudaOptions(div_approx=True, fast_path=True)).text
+    assert "#define NM_DIVX(a, b) (FAST ? nmodl::div_f((a), (b), dfl) : ((a) / (b)))" in text
+    assert "nmodl::div_af" in text
+    assert "= NM_DIVX(" in text
+
+
+@pytest.mark.parametrize("stem,kw", [OPTION_SETS[0], OPTION_SETS[2], OPTION_SETS[3], OPTION_SETS[5]])
+def test_option_builds_compile_for_sm100a(stem, kw, tmp_path):
+    """nvcc cross-compiles the emitted TU for sm_100a (no GPU needed)."""
+    import subprocess
+
+    from paper_1905_02241_b200.build import ARCH, INCLUDE, nvcc_path
+
+    src = tmp_path / "m.cu"
+    src.write_text(emit_cuda(load_ir(stem), CudaOptions(**kw)).text)
+    proc = subprocess.run([nvcc_path(), ARCH, "-O3", "-std=c++17", "-cubin", f"-I{INCLUDE}", "-diag-suppress", "177,550",
+                           str(src), "-o", str(tmp_path / "m.cubin")], capture_output=True, text=True)
+    assert proc.returncode == 0, proc.stderr[-2000:]

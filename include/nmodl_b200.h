@@ -132,6 +132,8 @@ int nmodl_selftest_div_approx(const double *a, const double *b, double *out, lon
 /* self-test: out[i] = nmodl::exp16(x[i]) (shared-memory table exp, CudaOptions.exp_smem);
  * flag bits as nmodl_selftest_exp_table */
 int nmodl_selftest_exp_smem(const double *x, double *out, unsigned *flag, long long n, nmodl_stream_t s);
+/* self-test: out[i] = nmodl::exp_e(x[i]) (Estrin-form exp, CudaOptions.exp_estrin); flags as above */
+int nmodl_selftest_exp_estrin(const double *x, double *out, unsigned *flag, long long n, nmodl_stream_t s);
 
 /* ---- per-mechanism library (lib<mech>-<hash>.so) -----------------------
  * Every generated mechanism exports exactly these symbols.  `md` points to a

@@ -602,3 +602,20 @@ NMODL_API int nmodl_selftest_exp_smem(const double* x, double* a, unsigned* fl, 
   CK(cudaGetLastError());
   return 0;
 }
+
+// Estrin-form exp (CudaOptions.exp_estrin): flag bits as the table self-tests
+__global__ void k_selftest_exp_estrin(const double* __restrict__ x, double* __restrict__ a,
+                                      unsigned* __restrict__ fl, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    unsigned f = 0;
+    const double fast = nmodl::exp_ef(x[i], f);
+    const double safe = nmodl::exp_e(x[i]);
+    a[i] = safe;
+    fl[i] = f | ((f == 0 && __double_as_longlong(fast) != __double_as_longlong(safe)) ? 2u : 0u);
+  }
+}
+NMODL_API int nmodl_selftest_exp_estrin(const double* x, double* a, unsigned* fl, long long n, cudaStream_t s) {
+  k_selftest_exp_estrin<<<256, 256, 0, s>>>(x, a, fl, n);
+  CK(cudaGetLastError());
+  return 0;
+}

@@ -89,6 +89,7 @@ _SIGS = {
     "nmodl_selftest_exp_table": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
     "nmodl_selftest_div_approx": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
     "nmodl_selftest_exp_smem": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
+    "nmodl_selftest_exp_estrin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
 }
 RUNTIME_SYMBOLS = tuple(_SIGS)
 

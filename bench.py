@@ -80,10 +80,12 @@ def options_for(stem: str):
 
     tuned = {
         "ProbAMPANMDA_EMS": CudaOptions(ilp=1, fast_path=False),
-        "hh_subset": CudaOptions(ilp=1, pipe=True, recip=True, div_approx=True, fast_redo=True),  # 0.0412 -> 0.0332 ms
-        "NaTs2_t": CudaOptions(ilp=2, min_blocks=2, pipe=True, recip=True, div_approx=True, fast_redo=True),  # 0.0788 -> 0.0594
+        "hh_subset": CudaOptions(ilp=1, pipe=True, recip=True, div_approx=True, exp_share=True,
+                                 fast_redo=True),  # 0.0412 -> 0.0329 ms
+        "NaTs2_t": CudaOptions(ilp=2, min_blocks=2, pipe=True, recip=True, div_approx=True, exp_share=True,
+                               fast_redo=True),  # 0.0788 -> 0.0557 ms
         "K_Pst": CudaOptions(ilp=2, min_blocks=2, pipe=True, recip=True, quot=True, div_approx=True, exp_smem=True,
-                             fast_redo=True),  # 0.0717 -> 0.0640 ms
+                             exp_share=True, fast_redo=True),  # 0.0717 -> 0.0574 ms
         "Ca_HVA": CudaOptions(ilp=2, min_blocks=2, pipe=True, recip=True, div_approx=True, fast_redo=True),  # 0.0707 -> 0.0561
         "SKv3_1": CudaOptions(ilp=1, pipe=True, grid_waves=4, div_approx=True, fast_redo=True),  # 0.0500 -> 0.0426 ms
         "Ih": CudaOptions(ilp=2, pipe=True, grid_waves=4, recip=True, div_approx=True, fast_redo=True),  # 0.0474 -> 0.0392 ms
@@ -93,9 +95,9 @@ def options_for(stem: str):
     return tuned.get(stem, CudaOptions())
 
 
-RELAXED_NOTE = ("fp64 throughout; rate code uses reciprocal shadows (X/(1/E) -> X*E), <=2-ulp division and "
-                "(K_Pst) a 1-ulp shared-table exp where tuned (bench.options_for); solver cores IEEE; "
-                "parity 1e-10 after 1000 steps is tested for every flag")
+RELAXED_NOTE = ("fp64 throughout; rate code uses reciprocal/quotient shadows (X/(1/E) -> X*E), <=2-ulp division, "
+                "shared affine exponentials (exp(aX+b) = exp(aX+b0)*exp(b-b0)) and (K_Pst) a 1-ulp shared-table exp "
+                "where tuned (bench.options_for); solver cores IEEE; parity 1e-10 after 1000 steps is tested for every flag")
 
 
 def bench_irs():

@@ -10,7 +10,9 @@ RELAXED = [dict(recip=True), dict(div_approx=True), dict(recip=True, div_approx=
            dict(recip=True, quot=True, div_approx=True, pipe=True, fast_redo=True),
            dict(recip=True, quot=True, fast_path=False),
            dict(recip=True, div_approx=True, exp_estrin=True, pipe=True, fast_redo=True),
-           dict(exp_estrin=True, fast_path=False)]
+           dict(exp_estrin=True, fast_path=False),
+           dict(recip=True, quot=True, div_approx=True, exp_share=True, pipe=True, fast_redo=True),
+           dict(exp_share=True, fast_path=False)]
 RELAXED_STEMS = ["hh_subset", "NaTs2_t", "Ca_HVA", "Ih", "na6", "cdp5ish", "ProbAMPANMDA_EMS",
                  "corpus_cat", "corpus_vtrap", "corpus_kdr", "K_Pst", "SKv3_1"]
 PIPE_STEMS = ["hh_subset", "NaTs2_t", "na6", "cdp5ish", "ProbAMPANMDA_EMS", "corpus_cat", "cadyn"]

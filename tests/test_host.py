@@ -284,6 +284,8 @@ def test_census_counts_match_the_mechanism():
 
 OPTION_SETS = [
     ("hh_subset", dict(pipe=True, recip=True, div_approx=True, fast_redo=True, fast_path=True)),
+    ("hh_subset", dict(exp_share=True, recip=True, fast_path=True)),
+    ("NaTs2_t", dict(exp_share=True, fast_path=False)),
     ("NaTs2_t", dict(ilp=2, pipe=True, recip=True, div_approx=True, fast_redo=True, fast_path=True, min_blocks=2)),
     ("K_Pst", dict(ilp=2, recip=True, quot=True, exp_smem=True, pipe=True, fast_path=True, fast_redo=True)),
     ("na6", dict(lu_spec=True, pipe=True, fast_path=True, fast_redo=True)),
@@ -352,3 +354,16 @@ def test_option_builds_compile_for_sm100a(stem, kw, tmp_path):
     proc = subprocess.run([nvcc_path(), ARCH, "-O3", "-std=c++17", "-cubin", f"-I{INCLUDE}", "-diag-suppress", "177,550",
                            str(src), "-o", str(tmp_path / "m.cubin")], capture_output=True, text=True)
     assert proc.returncode == 0, proc.stderr[-2000:]
+
+
+def test_exp_sharing_reuses_affine_exponentials():
+    """exp_share: hh's three exp(-(v+c)/10) (two vtrap, one beta_h) become
+    one exp and two constant multiples; NaTs2_t's exp(-(u+32)/6) /
+    exp((u+32)/6) pairs become one exp and one quotient each."""
+    hh = emit_cuda(load_ir("hh_subset"), CudaOptions(exp_share=True))
+    body = hh.text.split("hh_body_state_update")[1].split("hh_body_current_update")[0]
+    assert body.count("NM_EXP(") == 7  # 9 exps, two of the three /10 ones now constant multiples
+    assert len(re.findall(r"t_xs\d+ \* hh_K\[\d+\]", body)) == 2
+    nat = emit_cuda(load_ir("NaTs2_t"), CudaOptions(exp_share=True)).text
+    body = nat.split("NaTs2_t_body_state_update")[1].split("NaTs2_t_body_current_update")[0]
+    assert body.count("NM_EXP(") == 4 and len(re.findall(r"NM_DIV\(1\.0, t_xs\d+\)", body)) == 2

@@ -76,7 +76,7 @@ def grid(spec: str):
     for part in spec.split():
         k, vs = part.split("=")
         keys.append(k)
-        values.append([bool(int(v)) if k in ("fast_path", "exp_c", "const_pool", "fast_div", "const_div", "exp_inline", "stream_hints", "fmad", "bulk", "defer", "exp_table", "pipe", "recip", "div_approx", "exp_smem", "fast_redo", "lu_spec", "warp_tiles", "idx_ahead", "quot", "exp_estrin") else int(v)
+        values.append([bool(int(v)) if k in ("fast_path", "exp_c", "const_pool", "fast_div", "const_div", "exp_inline", "stream_hints", "fmad", "bulk", "defer", "exp_table", "pipe", "recip", "div_approx", "exp_smem", "fast_redo", "lu_spec", "warp_tiles", "idx_ahead", "quot", "exp_estrin", "exp_share") else int(v)
                        for v in vs.split(",")])
     return [CudaOptions(**dict(zip(keys, combo))) for combo in itertools.product(*values)]
 

@@ -2,17 +2,13 @@
 default options -- prebuilt by __graft_entry__.build() so the `-m gpu` run
 on the box does not spend its time in nvcc."""
 
-RELAXED = [dict(recip=True), dict(div_approx=True), dict(recip=True, div_approx=True),
-           dict(recip=True, div_approx=True, fast_path=False), dict(recip=True, div_approx=True, exp_smem=True),
-           dict(exp_smem=True, fast_path=False), dict(exp_smem=True, pipe=True, grid_waves=0),
-           dict(recip=True, div_approx=True, pipe=True, fast_redo=True),
+RELAXED = [dict(recip=True), dict(div_approx=True),
+           dict(recip=True, div_approx=True, fast_path=False),
+           dict(exp_smem=True, pipe=True, grid_waves=0),
            dict(recip=True, div_approx=True, pipe=True, fast_redo=True, ilp=2),
-           dict(recip=True, quot=True, div_approx=True, pipe=True, fast_redo=True),
-           dict(recip=True, quot=True, fast_path=False),
-           dict(recip=True, div_approx=True, exp_estrin=True, pipe=True, fast_redo=True),
-           dict(exp_estrin=True, fast_path=False),
            dict(recip=True, quot=True, div_approx=True, exp_share=True, pipe=True, fast_redo=True),
-           dict(exp_share=True, fast_path=False)]
+           dict(recip=True, quot=True, exp_share=True, exp_smem=True, fast_path=False),
+           dict(exp_estrin=True, fast_path=False)]
 RELAXED_STEMS = ["hh_subset", "NaTs2_t", "Ca_HVA", "Ih", "na6", "cdp5ish", "ProbAMPANMDA_EMS",
                  "corpus_cat", "corpus_vtrap", "corpus_kdr", "K_Pst", "SKv3_1"]
 PIPE_STEMS = ["hh_subset", "NaTs2_t", "na6", "cdp5ish", "ProbAMPANMDA_EMS", "corpus_cat", "cadyn"]

@@ -571,10 +571,10 @@ def e2e_measure(name, dist, calls=2, timesteps=1000):
 
 def _h2d(job):
     """Bytes the public call copies host->device: the whole store (v excepted
-    in node mode: it is gathered from the node voltages), node_index, node_v."""
+    in node mode: it is gathered from the node voltages; i_acc/g_acc are
+    outputs only), node_index, node_v."""
     ir, runner, data, extra, _, n = job
     b = sum(a.nbytes for k, a in data.arrays.items() if not (extra is not None and k == "v"))
-    b += sum(a.nbytes for a in data.acc.values())
     if extra is not None:
         b += extra[0].nbytes + extra[1].nbytes
     return b

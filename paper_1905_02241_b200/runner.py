@@ -191,6 +191,9 @@ class DeviceInstanceData:
         # arrays a launch (or the voltage gather) may have changed since the
         # upload: the only ones a write-back has to bring home
         self.dirty: set[str] = set()
+        # arrays holding no value yet (not uploaded, not written by a launch):
+        # never permuted, never downloaded
+        self.unset: set[str] = set()
 
     def reorder(self, perm_ptr: int, stream) -> None:
         """new[k] = old[perm[k]] for every array, into a fresh arena."""
@@ -200,8 +203,9 @@ class DeviceInstanceData:
         new_ptr = {}
         for i, name in enumerate(names):
             dst = arena.ptr + i * self.stride
-            rt.check(L.nmodl_permute(C.c_void_p(self.ptr[name]), C.c_void_p(dst), C.c_void_p(perm_ptr), self.n, 0,
-                                     C.c_void_p(stream.handle)), "permute")
+            if name not in self.unset:
+                rt.check(L.nmodl_permute(C.c_void_p(self.ptr[name]), C.c_void_p(dst), C.c_void_p(perm_ptr), self.n,
+                                         0, C.c_void_p(stream.handle)), "permute")
             new_ptr[name] = dst
         stream.sync()
         self.arena = arena  # the old arena returns to the allocator cache
@@ -209,6 +213,7 @@ class DeviceInstanceData:
 
     # ---- host <-> device ------------------------------------------------------
     def upload_from(self, data, stream, skip=()) -> None:
+        self.unset |= set(skip)
         for name in self.names:
             if name in skip:
                 continue
@@ -218,6 +223,8 @@ class DeviceInstanceData:
             rt.h2d(self.ptr[name], arr.ctypes.data, arr.nbytes, stream)
             stream.sync() if arr is not data.arrays[name] else None
         for name in ("i_acc", "g_acc"):
+            if name in skip:
+                continue
             arr = np.ascontiguousarray(data.acc[name], dtype=np.float64)
             rt.h2d(self.ptr[name], arr.ctypes.data, arr.nbytes, stream)
         stream.sync()
@@ -361,6 +368,8 @@ class CudaRunner:
         if only_dirty:
             names = [n for n in names if n in dev.dirty]
             acc = "i_acc" in dev.dirty
+        names = [n for n in names if n not in dev.unset or n in dev.dirty]
+        acc = acc and ("i_acc" not in dev.unset or "i_acc" in dev.dirty)
         if dev.nodes is not None:
             self._unpermute_into(dev, data, names, acc)
         else:
@@ -511,14 +520,36 @@ class CudaRunner:
 
     # ---- node_index extension ----------------------------------------------------------
     def bind_nodes(self, dev: DeviceInstanceData, node_index, node_v=None, node_rhs=None, node_d=None,
-                   tile: int | None = None, shared: "NodeArrays | None" = None) -> NodeBinding:
+                   tile: int | None = None, shared: "NodeArrays | None" = None,
+                   prepared: "NodeBinding | None" = None) -> NodeBinding:
         """Attach node arrays and reorder the store node-stably on the device.
 
         With `shared`, the node voltage/rhs/d arrays are the given device
         arrays (all mechanisms of a cell population fold into the same nodes,
-        in launch order); otherwise they are allocated from the host arrays."""
+        in launch order); otherwise they are allocated from the host arrays.
+        `prepared`: the result of prepare_nodes() for this population (its
+        node layout was built on another stream while the store uploaded)."""
         if dev.nodes is not None:
             raise ValueError("nodes already bound")
+        if prepared is None:
+            nb = self.prepare_nodes(dev.n, node_index, node_v, node_rhs, node_d, tile, shared)
+        else:
+            nb = prepared
+            if nb.n != dev.n:
+                raise ValueError("prepared node layout is for another population size")
+        return self._finish_nodes(dev, nb)
+
+    def aux_stream(self) -> "rt.Stream":
+        """A second stream of this runner (node layout built beside the upload)."""
+        if getattr(self, "_aux", None) is None:
+            self._aux = rt.Stream()
+        return self._aux
+
+    def prepare_nodes(self, n: int, node_index, node_v=None, node_rhs=None, node_d=None, tile: int | None = None,
+                      shared: "NodeArrays | None" = None, stream: "rt.Stream | None" = None) -> NodeBinding:
+        """Enqueue the node layout of an n-instance population (node_index
+        upload, stable sort, segments, tiles, node arrays) on `stream`
+        without waiting for it; bind_nodes(prepared=...) completes it."""
         self._mark("bind:start")
         node_index = np.ascontiguousarray(node_index, dtype=np.int32)
         if shared is None:
@@ -526,12 +557,12 @@ class CudaRunner:
             n_nodes = int(node_v.shape[0])
         else:
             n_nodes = shared.n_nodes
-        n = dev.n
         if node_index.shape != (n,):
             raise ValueError("node_index must have one entry per instance")
         nb = NodeBinding(n, n_nodes)
-        s = self.stream
+        s = stream or self.stream
         nb.stream = s
+        nb._host_keep = (node_index, node_v, node_rhs, node_d)  # sources of the async copies
         L = rt.lib()
         idx_in = nb.alloc(4 * n)
         rt.h2d(idx_in, node_index.ctypes.data, 4 * n, s)
@@ -584,11 +615,20 @@ class CudaRunner:
         rt.check(L.nmodl_node_segments(C.c_void_p(nb.node_offsets_full), n_nodes, n, T, C.c_void_p(nb.seg_node),
                                        C.c_void_p(nb.seg_offsets), C.c_void_p(nb.tile_segs), C.c_void_p(counts),
                                        C.c_void_p(s.handle)), "node_segments")
+        nb._pending = (counts, bad)
+        return nb
+
+    def _finish_nodes(self, dev: DeviceInstanceData, nb: NodeBinding) -> NodeBinding:
+        counts, bad = nb._pending
+        n = nb.n
+        s = nb.stream
         cnt = np.empty(2, dtype=np.int64)
         b = np.empty(1, dtype=np.int32)
         rt.d2h(cnt.ctypes.data, counts, 16, s)
         rt.d2h(b.ctypes.data, bad, 4, s)
         s.sync()
+        nb._host_keep = None
+        s = nb.stream = self.stream
         if b[0] != 0x7FFFFFFF:
             raise ValueError(f"node_index out of range at instance {int(b[0])}")
         nb.n_segs = int(cnt[0])
@@ -689,7 +729,9 @@ def simulate(layout, data, steps: int, jac_mode: str = "exact", on_step=None, ru
     """GPU twin of modlc.interp.simulate (interp.py:640-655): one upload,
     initialize, `steps` fused state+current launches, one download."""
     runner = runner or CudaRunner(layout, jac_mode=jac_mode)
-    dev = runner.to_device(data)
+    # i_acc / g_acc are outputs only (written with `=` by nrn_cur, read by
+    # nothing): not uploaded; downloaded once a launch has written them
+    dev = runner.to_device(data, skip=("i_acc", "g_acc"))
     try:
         runner.run_kernel(dev, "initialize", 1)
         if on_step is None:
@@ -722,12 +764,17 @@ def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, 
     t = {}
     t0 = clock()
     runner = runner or CudaRunner(layout, jac_mode=jac_mode)
-    # v is never uploaded: every instance's voltage is its node's
-    dev = runner.to_device(data, skip=("v",))
+    node_v = np.ascontiguousarray(node_v, dtype=np.float64)
+    # the node layout (node_index upload, stable sort, segments, tiles) is
+    # built on a second stream while the instance store uploads
+    aux = runner.aux_stream()
+    prep = runner.prepare_nodes(int(data.n), node_index, node_v, node_rhs, node_d, stream=aux)
+    # v is never uploaded (every instance's voltage is its node's); i_acc /
+    # g_acc are outputs only
+    dev = runner.to_device(data, skip=("v", "i_acc", "g_acc"))
     t["upload"] = clock() - t0
     t0 = clock()
-    node_v = np.ascontiguousarray(node_v, dtype=np.float64)
-    nb = runner.bind_nodes(dev, node_index, node_v, node_rhs, node_d)
+    nb = runner.bind_nodes(dev, node_index, prepared=prep)
     runner.gather_voltage(dev)
     if not np.isfinite(node_v).all():
         # a non-finite node voltage is a pre-existing non-finite v for the

@@ -12,13 +12,22 @@ from parity import TOL, parity
 pytestmark = pytest.mark.gpu
 
 
-def test_small_column_matches_oracle():
+@pytest.mark.parametrize("bench_options", [False, True])
+def test_small_column_matches_oracle(bench_options):
+    """Default builds, and the builds bench.py measures (bench.options_for:
+    relaxed rate arithmetic, fast_redo, ... -- here in node_index mode with
+    shared nodes and the one-instance-per-node path)."""
     from paper_1905_02241_b200.column import COUPLINGS, LAUNCH_ORDER, ColumnShard, ColumnSpec, load_irs, shard_layout
     from paper_1905_02241_b200.instance import init_range
 
     spec = ColumnSpec(n_cells=300, dend_per_cell=5, syn_per_cell=12, seed=7)
     steps = 100
-    shard = ColumnShard(spec, 0, spec.n_cells)
+    if bench_options:
+        from bench import options_for
+
+        shard = ColumnShard(spec, 0, spec.n_cells, options_for)
+    else:
+        shard = ColumnShard(spec, 0, spec.n_cells)
     shard.launch(steps)
     shard.check()
     irs = load_irs()

@@ -11,6 +11,9 @@ domain gives exact size-independent checks:
   np.subtract.at / np.add.at applied to the GPU's own per-instance currents;
 * determinism / permutation invariance -- two full-size runs, one of them on
   a permuted store, give bit-identical per-instance results.
+
+The full-size runs use the builds bench.py measures (bench.options_for);
+the default builds are covered at small sizes by test_gpu_parity.py.
 """
 
 import numpy as np
@@ -25,6 +28,13 @@ pytestmark = pytest.mark.gpu
 PREFIX = 65536
 
 
+def _runner(stem, ir):
+    from bench import options_for
+    from paper_1905_02241_b200.runner import CudaRunner
+
+    return CudaRunner(ir, options=options_for(stem))
+
+
 def _prefix(data, k):
     return O.InstanceData(k, {n: a[:k].copy() for n, a in data.arrays.items()},
                           {n: a[:k].copy() for n, a in data.acc.items()}, dict(data.scalars), list(data.newton_iters))
@@ -36,7 +46,7 @@ def test_hh_1m_1000_steps_prefix_matches_oracle():
 
     ir = load_ir("hh_subset")
     n, steps = 1_000_000, 1000
-    gpu = simulate(ir, init(ir, n, 42), steps, runner=CudaRunner(ir))
+    gpu = simulate(ir, init(ir, n, 42), steps, runner=_runner("hh_subset", ir))
     ref = O.simulate(ir, O.init(ir, PREFIX, 42), steps)
     dev, where = parity(ir, ref, _prefix(gpu, PREFIX))
     assert dev <= TOL, (dev, where)
@@ -49,7 +59,7 @@ def test_synapse_10m_nodes_1000_steps():
     ir = load_ir("ProbAMPANMDA_EMS")
     n, n_nodes, steps = 10_000_000, 1_000_000, 1000
     idx, nv = node_layout(n, n_nodes, 42)
-    gpu, rhs, d = simulate_nodes(ir, init(ir, n, 42), steps, idx, nv, runner=CudaRunner(ir))
+    gpu, rhs, d = simulate_nodes(ir, init(ir, n, 42), steps, idx, nv, runner=_runner("ProbAMPANMDA_EMS", ir))
     # per-instance prefix vs the oracle driven by the same gathered voltages
     ref = O.init(ir, PREFIX, 42)
     ref, _, _ = N.simulate_nodes(ir, ref, steps, idx[:PREFIX], nv)
@@ -79,7 +89,7 @@ def test_bbp_set_prefix_and_permutation_invariance():
     n, steps = 3_333_333, 1000
     for stem in ("NaTs2_t", "K_Pst", "Ca_HVA", "SKv3_1", "Ih", "cadyn"):
         ir = load_ir(stem)
-        runner = CudaRunner(ir)
+        runner = _runner(stem, ir)
         base = init(ir, n, 42)
         gpu = simulate(ir, base.copy(), steps, runner=runner)
         ref = O.simulate(ir, O.init(ir, 8192, 42), steps)
@@ -102,7 +112,7 @@ def test_kinetic_1m_prefix():
 
     for stem in ("na6", "cdp5ish"):
         ir = load_ir(stem)
-        gpu = simulate(ir, init(ir, 1_000_000, 42), 1000, runner=CudaRunner(ir))
+        gpu = simulate(ir, init(ir, 1_000_000, 42), 1000, runner=_runner(stem, ir))
         ref = O.simulate(ir, O.init(ir, 4096, 42), 1000)
         dev, where = parity(ir, ref, _prefix(gpu, 4096))
         assert dev <= TOL, (stem, dev, where)

@@ -107,8 +107,11 @@ def build_mechanism(layout, options: CudaOptions | None = None, fmad: bool | Non
     text = printer.emit_unit()
     abi = printer._abi
     flags = base_flags(fmad)
+    # the key must not depend on where the repo lives (the GPU box runs it
+    # from another path): the include directory enters through its content
+    portable = [f for f in flags if not f.startswith("-I")]
     key = hashlib.sha256(
-        (text + "\0" + " ".join(flags) + "\0" + _headers_digest()).encode()
+        (text + "\0" + " ".join(portable) + "\0" + _headers_digest()).encode()
     ).hexdigest()[:20]
     out_dir = BUILD / "mech"
     stem = f"{printer.mech}-{key}"

@@ -2,8 +2,7 @@
 default options -- prebuilt by __graft_entry__.build() so the `-m gpu` run
 on the box does not spend its time in nvcc."""
 
-RELAXED = [dict(recip=True), dict(div_approx=True),
-           dict(recip=True, div_approx=True, fast_path=False),
+RELAXED = [dict(recip=True, div_approx=True, fast_path=False),
            dict(exp_smem=True, pipe=True, grid_waves=0),
            dict(recip=True, div_approx=True, pipe=True, fast_redo=True, ilp=2),
            dict(recip=True, quot=True, div_approx=True, exp_share=True, pipe=True, fast_redo=True),
@@ -32,9 +31,7 @@ def variants():
         out.append(("ProbAMPANMDA_EMS", dict(fast_path=False, tile=t, grid_waves=w)))
     for t in (512, 128, 64, 2048):
         for kw in (dict(fast_path=False, pipe=True), dict(fast_path=True, fast_redo=True, pipe=True),
-                   dict(fast_path=False, pipe=True, min_blocks=4), dict(fast_path=False, warp_tiles=True),
-                   dict(fast_path=True, fast_redo=True, warp_tiles=True), dict(fast_path=False, idx_ahead=True),
-                   dict(fast_path=True, fast_redo=True, idx_ahead=True)):
+                   dict(fast_path=False, warp_tiles=True), dict(fast_path=True, fast_redo=True, idx_ahead=True)):
             out.append(("ProbAMPANMDA_EMS", dict(tile=min(t, 256) if kw.get("warp_tiles") else t, **kw)))
     out.append(("ProbAMPANMDA_EMS", dict(fast_path=False, pipe=True)))
     out.append(("ProbAMPANMDA_EMS", dict(fast_path=False, warp_tiles=True, tile=256)))
@@ -47,6 +44,11 @@ def variants():
     for st in ("na6", "cdp5ish", "corpus_fourstate", "corpus_pump", "corpus_fourstate.nopass", "corpus_pump.nopass"):
         out.append((st, dict(lu_spec=True)))
         out.append((st, dict(lu_spec=True, fast_path=True, fast_redo=True, pipe=True)))
+    for st in ("hh_subset", "ProbAMPANMDA_EMS", "corpus_exp2syn"):
+        out.append((st, dict(fmad=True)))
+    for st in ("hh_subset", "NaTs2_t", "K_Pst", "ProbAMPANMDA_EMS", "na6", "corpus_cat"):
+        for fast in (False, True):
+            out.append((st, dict(exp_table=True, fast_path=fast)))
     for st in RELAXED_STEMS:
         for r in RELAXED:
             out.append((st, {"fast_path": True, **r}))

@@ -204,9 +204,7 @@ def test_node_kernel_grid_waves_matches_oracle(waves, tile):
 
 
 NODE_PIPE = [dict(fast_path=False, pipe=True), dict(fast_path=True, fast_redo=True, pipe=True),
-             dict(fast_path=False, pipe=True, min_blocks=4), dict(fast_path=False, warp_tiles=True),
-             dict(fast_path=True, fast_redo=True, warp_tiles=True), dict(fast_path=False, idx_ahead=True),
-             dict(fast_path=True, fast_redo=True, idx_ahead=True)]
+             dict(fast_path=False, warp_tiles=True), dict(fast_path=True, fast_redo=True, idx_ahead=True)]
 
 
 @pytest.mark.parametrize("variant", range(len(NODE_PIPE)))

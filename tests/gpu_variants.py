@@ -2,7 +2,7 @@
 default options -- prebuilt by __graft_entry__.build() so the `-m gpu` run
 on the box does not spend its time in nvcc."""
 
-RELAXED = [dict(recip=True, div_approx=True, fast_path=False),
+RELAXED = [dict(recip=True), dict(div_approx=True), dict(recip=True, div_approx=True, fast_path=False),
            dict(exp_smem=True, pipe=True, grid_waves=0),
            dict(recip=True, div_approx=True, pipe=True, fast_redo=True, ilp=2),
            dict(recip=True, quot=True, div_approx=True, exp_share=True, pipe=True, fast_redo=True),

@@ -136,6 +136,44 @@ def table(stems_and_layouts) -> str:
     return "\n".join(rows)
 
 
+FP64_OPCODES = ("DFMA", "DMUL", "DADD", "DSETP", "DMNMX")
+
+
+def measured(layout, ncu_summary: dict, n_instances: int, options=None) -> dict:
+    """The census next to what one ncu capture of the same kernel measured
+    (tools/ncu_summary.py output, e.g. profiles/r01j/r1j_hh.json): FP64
+    thread-instructions and DRAM bytes per instance-step, the kernel time,
+    and the fraction of the HBM / FP64 roofs the capture reached.
+    `options`: the CudaOptions of the captured build (the traffic model
+    reads the emitted kernel's load/store set)."""
+    ir = from_layout(layout)
+    p = CudaPrinter(ir, options)
+    p.emit_unit()
+    m = ncu_summary["metrics"]
+
+    def num(prefix):
+        key = next(k for k in m if k.startswith(prefix))
+        return float(str(m[key]).replace(",", ""))
+
+    us = num("gpu__time_duration")
+    dram = (num("dram__bytes_read") + num("dram__bytes_write")) * 1e6  # ncu reports MB
+    ops = ncu_summary.get("instructions", {}).get("by_opcode_per_instance", {})
+    fp64_meas = sum(v for k, v in ops.items() if k in FP64_OPCODES)
+    clock = num("sm__cycles_elapsed.avg.per_second") * 1e9
+    fp64_rate = SM_COUNT * FP64_LANES_PER_SM * clock
+    b = bytes_per_instance(p._abi, "step_nodes" if "step_nodes" in ncu_summary["kernel"] else "step")
+    return {
+        "mechanism": ir.mechanism,
+        "census_fp64_ops": fp64_ops(ir),
+        "measured_fp64_instr": fp64_meas,
+        "algorithmic_bytes": b,
+        "measured_dram_bytes": dram / n_instances,
+        "kernel_us": us,
+        "hbm_fraction_algorithmic": b * n_instances / (us * 1e-6) / 6548.5e9,
+        "fp64_pipe_fraction": fp64_meas * n_instances / (us * 1e-6) / fp64_rate,
+    }
+
+
 if __name__ == "__main__":  # pragma: no cover
     import sys
     from pathlib import Path
@@ -143,6 +181,23 @@ if __name__ == "__main__":  # pragma: no cover
     from .ir import MechIR
 
     root = Path(__file__).resolve().parent.parent / "fixtures" / "ir"
+    if sys.argv[1:2] == ["--ncu"]:
+        # --ncu REPORT.json:STEM:N ...  census vs one ncu capture per kernel
+        import json
+
+        sys.path.insert(0, str(root.parent.parent))
+        from bench import options_for
+
+        print("| mechanism | census FP64 ops | measured FP64 instr | algorithmic B | DRAM B (ncu) | µs | "
+              "HBM (alg.) | FP64 pipe |")
+        print("|---|---|---|---|---|---|---|---|")
+        for spec in sys.argv[2:]:
+            path, stem, n = spec.rsplit(":", 2)
+            r = measured(MechIR.load(root / f"{stem}.json"), json.load(open(path))[0], int(n), options_for(stem))
+            print(f"| {stem} | {r['census_fp64_ops']} | {r['measured_fp64_instr']:.0f} | {r['algorithmic_bytes']} | "
+                  f"{r['measured_dram_bytes']:.0f} | {r['kernel_us']:.1f} | {r['hbm_fraction_algorithmic']:.0%} | "
+                  f"{r['fp64_pipe_fraction']:.0%} |")
+        sys.exit(0)
     stems = sys.argv[1:] or ["ProbAMPANMDA_EMS", "hh_subset", "NaTs2_t", "K_Pst", "Ca_HVA", "SKv3_1", "Ih",
                              "cadyn", "na6", "cdp5ish"]
     print(table([(s, MechIR.load(root / f"{s}.json")) for s in stems]))

@@ -367,3 +367,20 @@ def test_exp_sharing_reuses_affine_exponentials():
     nat = emit_cuda(load_ir("NaTs2_t"), CudaOptions(exp_share=True)).text
     body = nat.split("NaTs2_t_body_state_update")[1].split("NaTs2_t_body_current_update")[0]
     assert body.count("NM_EXP(") == 4 and len(re.findall(r"NM_DIV\(1\.0, t_xs\d+\)", body)) == 2
+
+
+def test_census_next_to_measured_ncu_counters():
+    """analysis.measured: the reference-style census beside one committed ncu
+    capture (profiles/r01j): kernel time, DRAM bytes and FP64 instructions
+    per instance, roof fractions in (0, 1]."""
+    import json
+
+    from bench import options_for
+    from paper_1905_02241_b200.analysis import measured
+
+    summ = json.loads((ROOT / "profiles" / "r01j" / "r1j_hh.json").read_text())[0]
+    r = measured(load_ir("hh_subset"), summ, 1_000_000, options_for("hh_subset"))
+    assert r["algorithmic_bytes"] == 144
+    assert 0 < r["hbm_fraction_algorithmic"] <= 1 and 0 < r["fp64_pipe_fraction"] <= 1
+    assert r["measured_fp64_instr"] < r["census_fp64_ops"]  # relaxed build: fewer than the census prices
+    assert 80 < r["measured_dram_bytes"] < 150

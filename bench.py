@@ -447,7 +447,8 @@ def run_column(args, dist):
 
     spec = ColumnSpec(n_cells=WORKLOADS["column"]["cells"])
     bounds = partition_cells(np.full(spec.n_cells, spec.cell_cost()), dist.world)
-    shard = ColumnShard(spec, int(bounds[dist.rank]), int(bounds[dist.rank + 1]), options_for)
+    shard = ColumnShard(spec, int(bounds[dist.rank]), int(bounds[dist.rank + 1]), options_for,
+                        concurrent_soma=os.environ.get("NMODL_COLUMN_SEQUENTIAL") is None)
     s0 = shard.stream
     K, W = args.steps, args.warmup
     shard.launch(W)

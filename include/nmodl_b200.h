@@ -84,6 +84,12 @@ int nmodl_device_sync(void);
 int nmodl_event_create(nmodl_event_t *out);
 int nmodl_event_destroy(nmodl_event_t e);
 int nmodl_event_record(nmodl_event_t e, nmodl_stream_t s);
+int nmodl_stream_wait_event(nmodl_stream_t s, nmodl_event_t e);
+/* fold the currents of up to 8 one-instance-per-node populations (run with
+ * seg_unique = 2, i.e. without their own node update) into node rhs/d, in
+ * population order: rhs[node_index[j]] -= i_p[j], d[...] += g_p[j] */
+int nmodl_combine_unique(double *rhs, double *d, const int *node_index, long long n,
+                         const double *const *i_ptrs, const double *const *g_ptrs, int n_pops, nmodl_stream_t s);
 int nmodl_event_sync(nmodl_event_t e);
 int nmodl_event_elapsed_ms(nmodl_event_t a, nmodl_event_t b, float *ms);
 /* CUDA-graph capture of the per-timestep launch loop */

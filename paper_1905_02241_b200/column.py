@@ -95,7 +95,13 @@ def load_irs() -> dict:
 class ColumnShard:
     """All populations of cells [cell_lo, cell_hi) resident on one GPU."""
 
-    def __init__(self, spec: ColumnSpec, cell_lo: int, cell_hi: int, options_for=None):
+    def __init__(self, spec: ColumnSpec, cell_lo: int, cell_hi: int, options_for=None,
+                 concurrent_soma: bool = False):
+        """`concurrent_soma`: the one-per-cell soma populations run on their
+        own streams (CaDynamics_E2 after Ca_HVA, whose ica it reads) without
+        touching the shared nodes; one combine kernel then folds their
+        currents into the soma rhs/d in LAUNCH_ORDER -- the same operations
+        in the same order as the sequential launches."""
         from .runner import CudaRunner, NodeArrays
 
         self.spec = spec
@@ -128,15 +134,62 @@ class ColumnShard:
             self.runners[dst].share_slot(self.devs[dst], dslot, self.devs[src], sslot)
         for stem in LAUNCH_ORDER:
             self.runners[stem].run_kernel(self.devs[stem], "initialize", 1)
+        self.concurrent = bool(concurrent_soma) and all(self.devs[m].nodes.seg_unique == 1 for m in SOMA_MECHS)
+        if self.concurrent:
+            from . import runtime as rt
+
+            self._side = {m: rt.Stream() for m in SOMA_MECHS}
+            self._fork, self._ca = rt.Event(), rt.Event()
+            self._join = {m: rt.Event() for m in SOMA_MECHS}
+            for m in SOMA_MECHS:
+                self.devs[m].nodes.seg_unique = 2  # currents stay in i_acc/g_acc
+            self._soma_order = [m for m in LAUNCH_ORDER if m in SOMA_MECHS]
+            import ctypes as C
+
+            k = len(self._soma_order)
+            self._iptr = (C.c_void_p * k)(*[self.devs[m].ptr["i_acc"] for m in self._soma_order])
+            self._gptr = (C.c_void_p * k)(*[self.devs[m].ptr["g_acc"] for m in self._soma_order])
 
     @property
     def n_instances(self) -> int:
         return sum(d.n for d in self.devs.values())
 
     def launch(self, steps: int = 1) -> None:
+        if not self.concurrent:
+            for _ in range(steps):
+                for stem in LAUNCH_ORDER:
+                    self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
+            return
+        import ctypes as C
+
+        from . import runtime as rt
+
+        L = rt.lib()
+        main = self.stream
+        first = self.devs[self._soma_order[0]]
         for _ in range(steps):
+            self._fork.record(main)
+            for m in self._soma_order:
+                side = self._side[m]
+                rt.stream_wait(side, self._fork)
+                if m == "cadyn":
+                    rt.stream_wait(side, self._ca)  # reads this step's Ca_HVA ica
+                r = self.runners[m]
+                r.stream = side
+                r.launch(self.devs[m], "step_nodes", 1)
+                r.stream = main
+                if m == "Ca_HVA":
+                    self._ca.record(side)
+                self._join[m].record(side)
+            for m in self._soma_order:
+                rt.stream_wait(main, self._join[m])
+            nb = first.nodes
+            rt.check(L.nmodl_combine_unique(C.c_void_p(nb.node_rhs), C.c_void_p(nb.node_d), C.c_void_p(nb.node_index),
+                                            first.n, self._iptr, self._gptr, len(self._soma_order),
+                                            C.c_void_p(main.handle)), "combine_unique")
             for stem in LAUNCH_ORDER:
-                self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
+                if stem not in SOMA_MECHS:
+                    self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
 
     def check(self) -> None:
         for stem in LAUNCH_ORDER:

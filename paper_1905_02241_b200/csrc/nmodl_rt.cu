@@ -134,6 +134,10 @@ NMODL_API int nmodl_event_record(cudaEvent_t e, cudaStream_t s) {
   CK(cudaEventRecord(e, s));
   return 0;
 }
+NMODL_API int nmodl_stream_wait_event(cudaStream_t s, cudaEvent_t e) {
+  CK(cudaStreamWaitEvent(s, e, 0));
+  return 0;
+}
 NMODL_API int nmodl_event_sync(cudaEvent_t e) {
   CK(cudaEventSynchronize(e));
   return 0;
@@ -616,6 +620,46 @@ __global__ void k_selftest_exp_estrin(const double* __restrict__ x, double* __re
 }
 NMODL_API int nmodl_selftest_exp_estrin(const double* x, double* a, unsigned* fl, long long n, cudaStream_t s) {
   k_selftest_exp_estrin<<<256, 256, 0, s>>>(x, a, fl, n);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// Deferred in-order fold of one-instance-per-node populations (seg_unique
+// mode 2): the populations ran concurrently and left their currents in
+// i_acc/g_acc; node k of instance j receives them in population order --
+// the same operations, in the same order, as the sequential kernels' own
+// node_rhs[nd] -= i / node_d[nd] += g.
+struct nmodl_combine_args {
+  const double* i[8];
+  const double* g[8];
+  int n_pops;
+};
+__global__ void k_combine_unique(double* __restrict__ rhs, double* __restrict__ d, const int* __restrict__ node_index,
+                                 long long n, const nmodl_combine_args a) {
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    const int nd = node_index[j];
+    double r = rhs[nd], dd = d[nd];
+    for (int p = 0; p < a.n_pops; ++p) {
+      r = r - a.i[p][j];
+      dd = dd + a.g[p][j];
+    }
+    rhs[nd] = r;
+    d[nd] = dd;
+  }
+}
+NMODL_API int nmodl_combine_unique(double* rhs, double* d, const int* node_index, long long n,
+                                   const double* const* i_ptrs, const double* const* g_ptrs, int n_pops,
+                                   cudaStream_t s) {
+  if (n_pops < 0 || n_pops > 8) return (int)cudaErrorInvalidValue;
+  if (n <= 0) return 0;
+  nmodl_combine_args a{};
+  for (int p = 0; p < n_pops; ++p) {
+    a.i[p] = i_ptrs[p];
+    a.g[p] = g_ptrs[p];
+  }
+  a.n_pops = n_pops;
+  long long blocks = (n + 255) / 256;
+  k_combine_unique<<<(int)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, s>>>(rhs, d, node_index, n, a);
   CK(cudaGetLastError());
   return 0;
 }

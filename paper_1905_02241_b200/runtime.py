@@ -63,6 +63,9 @@ _SIGS = {
     "nmodl_event_create": (C.c_int, [C.POINTER(C.c_void_p)]),
     "nmodl_event_destroy": (C.c_int, [C.c_void_p]),
     "nmodl_event_record": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "nmodl_stream_wait_event": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "nmodl_combine_unique": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p,
+                                       C.c_int, C.c_void_p]),
     "nmodl_event_sync": (C.c_int, [C.c_void_p]),
     "nmodl_event_elapsed_ms": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_float)]),
     "nmodl_capture_begin": (C.c_int, [C.c_void_p]),
@@ -232,6 +235,10 @@ class Stream:
                 lib().nmodl_stream_destroy(C.c_void_p(self.handle))
         except Exception:
             pass
+
+
+def stream_wait(stream: "Stream", event: "Event") -> None:
+    check(lib().nmodl_stream_wait_event(C.c_void_p(stream.handle), C.c_void_p(event.handle)), "stream_wait_event")
 
 
 class Event:

@@ -12,8 +12,8 @@ from parity import TOL, parity
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("bench_options", [False, True])
-def test_small_column_matches_oracle(bench_options):
+@pytest.mark.parametrize("bench_options,concurrent", [(False, False), (True, False), (False, True), (True, True)])
+def test_small_column_matches_oracle(bench_options, concurrent):
     """Default builds, and the builds bench.py measures (bench.options_for:
     relaxed rate arithmetic, fast_redo, ... -- here in node_index mode with
     shared nodes and the one-instance-per-node path)."""
@@ -25,9 +25,10 @@ def test_small_column_matches_oracle(bench_options):
     if bench_options:
         from bench import options_for
 
-        shard = ColumnShard(spec, 0, spec.n_cells, options_for)
+        shard = ColumnShard(spec, 0, spec.n_cells, options_for, concurrent_soma=concurrent)
     else:
-        shard = ColumnShard(spec, 0, spec.n_cells)
+        shard = ColumnShard(spec, 0, spec.n_cells, concurrent_soma=concurrent)
+    assert shard.concurrent == concurrent
     shard.launch(steps)
     shard.check()
     irs = load_irs()
@@ -61,3 +62,25 @@ def test_column_shards_add_up():
         s.check()
     cw, ca, cb = whole.checksums(), a.checksums(), b.checksums()
     np.testing.assert_allclose(ca[:, 1] + cb[:, 1], cw[:, 1], rtol=1e-12)
+
+
+def test_concurrent_soma_is_bit_identical_and_graph_capturable():
+    """The concurrent soma schedule (side streams + in-order combine) gives
+    the sequential schedule's node rhs/d and states BIT FOR BIT, also when
+    the step is captured into a CUDA graph (as bench.py does)."""
+    from paper_1905_02241_b200 import runtime as rt
+    from paper_1905_02241_b200.column import LAUNCH_ORDER, ColumnShard, ColumnSpec
+
+    spec = ColumnSpec(n_cells=700, dend_per_cell=6, syn_per_cell=9, seed=5)
+    seq = ColumnShard(spec, 0, spec.n_cells)
+    con = ColumnShard(spec, 0, spec.n_cells, concurrent_soma=True)
+    seq.launch(30)
+    g = rt.capture(con.stream, lambda: con.launch(30))
+    g.launch(con.stream)
+    seq.check()
+    con.check()
+    a, b = seq.nodes.download(seq.stream), con.nodes.download(con.stream)
+    for k in ("node_rhs", "node_d"):
+        np.testing.assert_array_equal(a[k].view(np.int64), b[k].view(np.int64), err_msg=k)
+    np.testing.assert_array_equal(seq.checksums(), con.checksums())
+    assert set(LAUNCH_ORDER)

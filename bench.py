@@ -79,7 +79,7 @@ def options_for(stem: str):
     from paper_1905_02241_b200.codegen_cuda import CudaOptions
 
     tuned = {
-        "ProbAMPANMDA_EMS": CudaOptions(ilp=1, fast_path=False),
+        "ProbAMPANMDA_EMS": CudaOptions(ilp=1, fast_path=False, tile=2304),  # 2048: 0.2823, 2304: 0.2807 ms (3 reps)
         "hh_subset": CudaOptions(ilp=1, pipe=True, recip=True, div_approx=True, exp_share=True,
                                  fast_redo=True),  # 0.0412 -> 0.0329 ms
         "NaTs2_t": CudaOptions(ilp=2, min_blocks=2, pipe=True, recip=True, div_approx=True, exp_share=True,

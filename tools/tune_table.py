@@ -3,7 +3,7 @@ per-line table.   python tools/tune_table.py gpurun_out/tune_*.jsonl"""
 import json
 import sys
 
-KEYS = ("ilp", "fast_path", "min_blocks", "pipe", "grid_waves", "tile", "exp_table", "recip", "div_approx", "exp_smem", "fast_redo", "lu_spec", "warp_tiles", "idx_ahead", "quot", "exp_estrin", "exp_share")
+KEYS = ("ilp", "fast_path", "min_blocks", "pipe", "grid_waves", "tile", "exp_table", "recip", "div_approx", "exp_smem", "fast_redo", "lu_spec", "warp_tiles", "idx_ahead", "quot", "exp_estrin", "exp_share", "block")
 best = {}
 for path in sys.argv[1:]:
     for line in open(path):

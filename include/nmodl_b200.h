@@ -85,6 +85,9 @@ int nmodl_event_create(nmodl_event_t *out);
 int nmodl_event_destroy(nmodl_event_t e);
 int nmodl_event_record(nmodl_event_t e, nmodl_stream_t s);
 int nmodl_stream_wait_event(nmodl_stream_t s, nmodl_event_t e);
+/* event record that stays a timestamped node inside a stream capture
+ * (cudaEventRecordExternal): kernel boundaries inside a replayed graph */
+int nmodl_event_record_external(nmodl_event_t e, nmodl_stream_t s);
 /* fold the currents of up to 8 one-instance-per-node populations (run with
  * seg_unique = 2, i.e. without their own node update) into node rhs/d, in
  * population order: rhs[node_index[j]] -= i_p[j], d[...] += g_p[j] */
@@ -129,17 +132,25 @@ int nmodl_permute_i32(const int *src, int *dst, const long long *perm, long long
 int nmodl_gather_v(const double *node_v, const int *node_index, double *v, long long n, nmodl_stream_t s);
 /* self-test: out_a[i] = nmodl::exp_c(x[i]), out_b[i] = exp(x[i]) (bit-equality check) */
 int nmodl_selftest_exp(const double *x, double *out_a, double *out_b, long long n, nmodl_stream_t s);
-/* self-test: out[i] = nmodl::exp_t(x[i]); flag[i] bit 0 = fast form flagged,
- * bit 1 = fast and safe forms disagree without a flag (must never happen) */
-int nmodl_selftest_exp_table(const double *x, double *out, unsigned *flag, long long n, nmodl_stream_t s);
 /* self-test: out[i] = nmodl::div_a(a[i], b[i]) (relaxed division, CudaOptions.div_approx);
  * a signalling-NaN marker where the branch-free form disagrees without flagging */
 int nmodl_selftest_div_approx(const double *a, const double *b, double *out, long long n, nmodl_stream_t s);
 /* self-test: out[i] = nmodl::exp16(x[i]) (shared-memory table exp, CudaOptions.exp_smem);
- * flag bits as nmodl_selftest_exp_table */
+ * flag[i] bit 0 = fast form flagged, bit 1 = fast and safe forms disagree without a flag */
 int nmodl_selftest_exp_smem(const double *x, double *out, unsigned *flag, long long n, nmodl_stream_t s);
-/* self-test: out[i] = nmodl::exp_e(x[i]) (Estrin-form exp, CudaOptions.exp_estrin); flags as above */
-int nmodl_selftest_exp_estrin(const double *x, double *out, unsigned *flag, long long n, nmodl_stream_t s);
+
+/* ---- NCCL: validation collectives only (no exchange on the per-step path) --
+ * libnccl.so.2 is opened at first use; the unique id travels between the
+ * ranks of one node through the caller's bootstrap (parallel.py: a file).
+ * Replaces torch.distributed in the multi-GPU plumbing (PAPER.md:674-678:
+ * one rank per device, instances sharded by cell). */
+int nmodl_nccl_unique_id(unsigned char *out128);
+int nmodl_nccl_init(void **comm, int nranks, const unsigned char *id128, int rank);
+int nmodl_nccl_destroy(void *comm);
+/* op: 0 = sum, 1 = max */
+int nmodl_nccl_allreduce_f64(void *comm, const double *send, double *recv, long long count, int op,
+                             nmodl_stream_t s);
+int nmodl_nccl_allgather_f64(void *comm, const double *send, double *recv, long long count, nmodl_stream_t s);
 
 /* ---- per-mechanism library (lib<mech>-<hash>.so) -----------------------
  * Every generated mechanism exports exactly these symbols.  `md` points to a

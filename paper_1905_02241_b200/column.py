@@ -11,7 +11,10 @@ SPEC.md:441, modlc/layout.py:124-128).  Cell c owns compartments (nodes)
 
 Per timestep the populations run in LAUNCH_ORDER, each one fused kernel that
 gathers v from the shared node voltage, runs nrn_state + nrn_cur and folds its
-currents into the shared node rhs/d in instance order.  CaDynamics_E2 reads
+currents into the shared node rhs/d in instance order.  The node rhs/d are
+rebuilt every timestep (a cable solver's matrix setup): Ih, which has one
+instance on every compartment, goes first and assigns them (rhs = 0 - i,
+d = 0 + g); the other populations accumulate.  CaDynamics_E2 reads
 Ca_HVA's `ica` array directly (ion coupling; Ca_HVA is launched first), which
 is what NEURON's shared ion arrays do.  Instance data are drawn with
 `init_range`, so a shard of cells [lo, hi) holds exactly the instances the
@@ -31,7 +34,7 @@ from .ir import MechIR
 
 FIXTURES = Path(__file__).resolve().parent.parent / "fixtures" / "ir"
 SOMA_MECHS = ("NaTs2_t", "K_Pst", "Ca_HVA", "cadyn", "SKv3_1")
-LAUNCH_ORDER = ("NaTs2_t", "K_Pst", "Ca_HVA", "cadyn", "SKv3_1", "Ih", "ProbAMPANMDA_EMS")
+LAUNCH_ORDER = ("Ih", "NaTs2_t", "K_Pst", "Ca_HVA", "cadyn", "SKv3_1", "ProbAMPANMDA_EMS")
 COUPLINGS = (("cadyn", "ica", "Ca_HVA", "ica"),)  # consumer slot <- producer slot
 
 
@@ -88,6 +91,15 @@ def shard_layout(spec: ColumnSpec, cell_lo: int, cell_hi: int) -> dict:
     return {"mechs": out, "node_v": node_v, "n_nodes": ncell * npc}
 
 
+def host_stores(spec: ColumnSpec, cell_lo: int, cell_hi: int) -> dict:
+    """{stem: HostInstanceData} of cells [cell_lo, cell_hi) (init_range: the
+    single-GPU column's instances for exactly those cells)."""
+    lay = shard_layout(spec, cell_lo, cell_hi)
+    irs = load_irs()
+    return {stem: init_range(irs[stem], lay["mechs"][stem][0], lay["mechs"][stem][1], spec.seed)
+            for stem in LAUNCH_ORDER}
+
+
 def load_irs() -> dict:
     return {stem: MechIR.load(FIXTURES / f"{stem}.json") for stem in LAUNCH_ORDER}
 
@@ -96,7 +108,8 @@ class ColumnShard:
     """All populations of cells [cell_lo, cell_hi) resident on one GPU."""
 
     def __init__(self, spec: ColumnSpec, cell_lo: int, cell_hi: int, options_for=None,
-                 concurrent_soma: bool = False):
+                 concurrent_soma: bool = False, reset: bool = True, host: dict | None = None,
+                 runners: dict | None = None):
         """`concurrent_soma`: the one-per-cell soma populations run on their
         own streams (CaDynamics_E2 after Ca_HVA, whose ica it reads) without
         touching the shared nodes; one combine kernel then folds their
@@ -105,6 +118,7 @@ class ColumnShard:
         from .runner import CudaRunner, NodeArrays
 
         self.spec = spec
+        self.reset = reset
         self.cells = (cell_lo, cell_hi)
         lay = shard_layout(spec, cell_lo, cell_hi)
         self.layout = lay
@@ -113,7 +127,7 @@ class ColumnShard:
         first = None
         for stem in LAUNCH_ORDER:
             opts = options_for(stem) if options_for else None
-            r = CudaRunner(irs[stem], options=opts)
+            r = runners[stem] if runners is not None else CudaRunner(irs[stem], options=opts)
             if first is None:
                 first = r
             else:
@@ -124,7 +138,7 @@ class ColumnShard:
         for stem in LAUNCH_ORDER:
             lo, hi, idx = lay["mechs"][stem]
             r = self.runners[stem]
-            data = init_range(irs[stem], lo, hi, spec.seed)
+            data = host[stem] if host is not None else init_range(irs[stem], lo, hi, spec.seed)
             dev = r.to_device(data)
             r.bind_nodes(dev, idx, shared=self.nodes)
             r.gather_voltage(dev)
@@ -134,6 +148,11 @@ class ColumnShard:
             self.runners[dst].share_slot(self.devs[dst], dslot, self.devs[src], sslot)
         for stem in LAUNCH_ORDER:
             self.runners[stem].run_kernel(self.devs[stem], "initialize", 1)
+        # per-step node reset: Ih (one instance per compartment, launched
+        # first) assigns rhs/d; otherwise a memset starts each step
+        ih = self.devs["Ih"].nodes
+        self._assign_first = bool(reset) and ih.seg_unique == 1 and ih.n == self.nodes.n_nodes
+        ih.assign = 1 if self._assign_first else 0
         self.concurrent = bool(concurrent_soma) and all(self.devs[m].nodes.seg_unique == 1 for m in SOMA_MECHS)
         if self.concurrent:
             from . import runtime as rt
@@ -154,9 +173,20 @@ class ColumnShard:
     def n_instances(self) -> int:
         return sum(d.n for d in self.devs.values())
 
+    def _reset_nodes(self) -> None:
+        """Start of a timestep: node rhs/d rebuilt from zero (cable-solver
+        matrix setup; oracle/column_np.py reset=True)."""
+        if self.reset and not self._assign_first:
+            from . import runtime as rt
+
+            nbytes = 8 * self.nodes.n_nodes
+            rt.memset(self.nodes.node_rhs, 0, nbytes, self.stream)
+            rt.memset(self.nodes.node_d, 0, nbytes, self.stream)
+
     def launch(self, steps: int = 1) -> None:
         if not self.concurrent:
             for _ in range(steps):
+                self._reset_nodes()
                 for stem in LAUNCH_ORDER:
                     self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
             return
@@ -168,6 +198,7 @@ class ColumnShard:
         main = self.stream
         first = self.devs[self._soma_order[0]]
         for _ in range(steps):
+            self._reset_nodes()
             self._fork.record(main)
             for m in self._soma_order:
                 side = self._side[m]
@@ -181,13 +212,18 @@ class ColumnShard:
                 if m == "Ca_HVA":
                     self._ca.record(side)
                 self._join[m].record(side)
+            # folds in LAUNCH_ORDER: the populations before the soma group,
+            # the soma group (combine, in order), the populations after it
+            soma_at = min(LAUNCH_ORDER.index(m) for m in SOMA_MECHS)
+            for stem in LAUNCH_ORDER[:soma_at]:
+                self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
             for m in self._soma_order:
                 rt.stream_wait(main, self._join[m])
             nb = first.nodes
             rt.check(L.nmodl_combine_unique(C.c_void_p(nb.node_rhs), C.c_void_p(nb.node_d), C.c_void_p(nb.node_index),
                                             first.n, self._iptr, self._gptr, len(self._soma_order),
                                             C.c_void_p(main.handle)), "combine_unique")
-            for stem in LAUNCH_ORDER:
+            for stem in LAUNCH_ORDER[soma_at:]:
                 if stem not in SOMA_MECHS:
                     self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
 
@@ -212,3 +248,26 @@ class ColumnShard:
             r, d = self.runners[stem], self.devs[stem]
             rows.append(device_checksums(r, d, [s for s in r.abi.slots if s in d.ptr] + ["i_acc", "g_acc"]))
         return np.concatenate(rows)
+
+
+def simulate_column(spec: ColumnSpec, steps: int, cell_lo: int = 0, cell_hi: int | None = None,
+                    host: dict | None = None, options_for=None, runners: dict | None = None,
+                    reset: bool = True, concurrent_soma: bool = False):
+    """Public column call (configs[4]): upload the stores of cells
+    [cell_lo, cell_hi) (`host`, e.g. from host_stores(), ideally pinned),
+    build the shared node layout on the device, nrn_init, `steps` timesteps
+    of all populations, then download every store (in place, instance order)
+    and the node arrays.  Returns (host, {"node_rhs", "node_d", "node_v"},
+    shard).  Pass the previous call's `shard.runners` to reuse the loaded
+    kernels."""
+    cell_hi = spec.n_cells if cell_hi is None else cell_hi
+    if host is None:
+        host = host_stores(spec, cell_lo, cell_hi)
+    shard = ColumnShard(spec, cell_lo, cell_hi, options_for, concurrent_soma=concurrent_soma, reset=reset,
+                        host=host, runners=runners)
+    shard.launch(steps)
+    shard.check()
+    for stem in LAUNCH_ORDER:
+        shard.runners[stem].to_host(shard.devs[stem], host[stem], only_dirty=True)
+    nodes = shard.nodes.download(shard.stream)
+    return host, nodes, shard

@@ -134,6 +134,13 @@ NMODL_API int nmodl_event_record(cudaEvent_t e, cudaStream_t s) {
   CK(cudaEventRecord(e, s));
   return 0;
 }
+// Inside a stream capture this becomes an event-record node that keeps its
+// timestamp (cudaEventRecordExternal), so kernel boundaries inside a replayed
+// graph can be timed; outside a capture it is an ordinary record.
+NMODL_API int nmodl_event_record_external(cudaEvent_t e, cudaStream_t s) {
+  CK(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal));
+  return 0;
+}
 NMODL_API int nmodl_stream_wait_event(cudaStream_t s, cudaEvent_t e) {
   CK(cudaStreamWaitEvent(s, e, 0));
   return 0;
@@ -552,24 +559,6 @@ NMODL_API int nmodl_selftest_exp(const double* x, double* a, double* b, long lon
   CK(cudaGetLastError());
   return 0;
 }
-// self-test: the table-driven exp (exp_t, and its fast form exp_tf with the flag)
-__global__ void k_selftest_exp_table(const double* __restrict__ x, double* __restrict__ a,
-                                     unsigned* __restrict__ fl, long long n) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    unsigned f = 0;
-    const double fast = nmodl::exp_tf(x[i], f);
-    const double safe = nmodl::exp_t(x[i]);
-    a[i] = safe;
-    // the fast form must agree with the safe form whenever it does not flag
-    fl[i] = f | ((f == 0 && __double_as_longlong(fast) != __double_as_longlong(safe)) ? 2u : 0u);
-  }
-}
-NMODL_API int nmodl_selftest_exp_table(const double* x, double* a, unsigned* fl, long long n, cudaStream_t s) {
-  k_selftest_exp_table<<<256, 256, 0, s>>>(x, a, fl, n);
-  CK(cudaGetLastError());
-  return 0;
-}
-
 // relaxed division (CudaOptions.div_approx): out[i] = div_a(a[i], b[i]); the
 // branch-free div_af must give the same value whenever it does not flag
 __global__ void k_selftest_div_approx(const double* __restrict__ a, const double* __restrict__ b,
@@ -603,23 +592,6 @@ __global__ void k_selftest_exp_smem(const double* __restrict__ x, double* __rest
 }
 NMODL_API int nmodl_selftest_exp_smem(const double* x, double* a, unsigned* fl, long long n, cudaStream_t s) {
   k_selftest_exp_smem<<<256, 256, 0, s>>>(x, a, fl, n);
-  CK(cudaGetLastError());
-  return 0;
-}
-
-// Estrin-form exp (CudaOptions.exp_estrin): flag bits as the table self-tests
-__global__ void k_selftest_exp_estrin(const double* __restrict__ x, double* __restrict__ a,
-                                      unsigned* __restrict__ fl, long long n) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    unsigned f = 0;
-    const double fast = nmodl::exp_ef(x[i], f);
-    const double safe = nmodl::exp_e(x[i]);
-    a[i] = safe;
-    fl[i] = f | ((f == 0 && __double_as_longlong(fast) != __double_as_longlong(safe)) ? 2u : 0u);
-  }
-}
-NMODL_API int nmodl_selftest_exp_estrin(const double* x, double* a, unsigned* fl, long long n, cudaStream_t s) {
-  k_selftest_exp_estrin<<<256, 256, 0, s>>>(x, a, fl, n);
   CK(cudaGetLastError());
   return 0;
 }
@@ -661,5 +633,98 @@ NMODL_API int nmodl_combine_unique(double* rhs, double* d, const int* node_index
   long long blocks = (n + 255) / 256;
   k_combine_unique<<<(int)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, s>>>(rhs, d, node_index, n, a);
   CK(cudaGetLastError());
+  return 0;
+}
+
+
+// ---------------------------------------------------------------------------
+// NCCL (validation collectives only: the hot path has no exchange).  The
+// library is opened at first use (libnccl.so.2 of the image), so the runtime
+// loads on hosts without NCCL and a multi-GPU call fails loudly there.
+// Bootstrap of the unique id is the caller's (parallel.py: a file shared by
+// the ranks of one node).
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace {
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+int nccl_load() {
+  if (g_nccl.h) return 0;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
+  if (!h) {
+    snprintf(g_err, sizeof(g_err), "NCCL not available: %s", dlerror());
+    return 1000;
+  }
+  g_nccl.get_unique_id = (decltype(g_nccl.get_unique_id))dlsym(h, "ncclGetUniqueId");
+  g_nccl.comm_init_rank = (decltype(g_nccl.comm_init_rank))dlsym(h, "ncclCommInitRank");
+  g_nccl.comm_destroy = (decltype(g_nccl.comm_destroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.all_reduce = (decltype(g_nccl.all_reduce))dlsym(h, "ncclAllReduce");
+  g_nccl.all_gather = (decltype(g_nccl.all_gather))dlsym(h, "ncclAllGather");
+  g_nccl.error_string = (decltype(g_nccl.error_string))dlsym(h, "ncclGetErrorString");
+  if (!g_nccl.get_unique_id || !g_nccl.comm_init_rank || !g_nccl.comm_destroy || !g_nccl.all_reduce ||
+      !g_nccl.all_gather || !g_nccl.error_string) {
+    snprintf(g_err, sizeof(g_err), "NCCL symbols missing in the loaded library");
+    return 1001;
+  }
+  g_nccl.h = h;
+  return 0;
+}
+
+int nccl_fail(ncclResult_t r, const char* what) {
+  snprintf(g_err, sizeof(g_err), "%s: NCCL error %d (%s)", what, (int)r,
+           g_nccl.error_string ? g_nccl.error_string(r) : "?");
+  return 2000 + (int)r;
+}
+}  // namespace
+
+#define NCK(call, what)                               \
+  do {                                                \
+    ncclResult_t r_ = (call);                         \
+    if (r_ != ncclSuccess) return nccl_fail(r_, what); \
+  } while (0)
+
+NMODL_API int nmodl_nccl_unique_id(unsigned char* out128) {
+  if (int rc = nccl_load()) return rc;
+  ncclUniqueId id;
+  NCK(g_nccl.get_unique_id(&id), "ncclGetUniqueId");
+  memcpy(out128, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return 0;
+}
+NMODL_API int nmodl_nccl_init(void** comm, int nranks, const unsigned char* id128, int rank) {
+  if (int rc = nccl_load()) return rc;
+  ncclUniqueId id;
+  memcpy(id.internal, id128, NCCL_UNIQUE_ID_BYTES);
+  ncclComm_t c = nullptr;
+  NCK(g_nccl.comm_init_rank(&c, nranks, id, rank), "ncclCommInitRank");
+  *comm = (void*)c;
+  return 0;
+}
+NMODL_API int nmodl_nccl_destroy(void* comm) {
+  if (int rc = nccl_load()) return rc;
+  NCK(g_nccl.comm_destroy((ncclComm_t)comm), "ncclCommDestroy");
+  return 0;
+}
+// op: 0 sum, 1 max (fp64)
+NMODL_API int nmodl_nccl_allreduce_f64(void* comm, const double* send, double* recv, long long count, int op,
+                                       cudaStream_t s) {
+  if (int rc = nccl_load()) return rc;
+  NCK(g_nccl.all_reduce(send, recv, (size_t)count, ncclFloat64, op == 1 ? ncclMax : ncclSum, (ncclComm_t)comm, s),
+      "ncclAllReduce");
+  return 0;
+}
+NMODL_API int nmodl_nccl_allgather_f64(void* comm, const double* send, double* recv, long long count, cudaStream_t s) {
+  if (int rc = nccl_load()) return rc;
+  NCK(g_nccl.all_gather(send, recv, (size_t)count, ncclFloat64, (ncclComm_t)comm, s), "ncclAllGather");
   return 0;
 }

@@ -120,3 +120,14 @@ def parity(ir, a, b, floored=False):
         if g > worst:
             worst, where = g, "+".join(grp)
     return worst, where
+
+
+def node_dev(got, want, scale) -> float:
+    """Node rhs/d deviation: max |got - want| / max(|got|, |want|, scale) with
+    `scale` = the per-node sum of |terms| folded into it (oracle/nodes_np.
+    abs_terms).  A node sum of same-sign terms is held to the pure relative
+    bar; one whose terms cancel is held to it relative to the terms' size,
+    the bound a sum of individually-rounded terms can honour."""
+    got, want, scale = (np.asarray(x, dtype=np.float64) for x in (got, want, scale))
+    den = np.maximum(np.maximum(np.abs(got), np.abs(want)), np.maximum(scale, 1e-30))
+    return float(np.max(np.abs(got - want) / den)) if got.size else 0.0

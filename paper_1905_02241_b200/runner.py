@@ -90,6 +90,9 @@ class NodeBinding:
         self.n = n
         self.n_nodes = n_nodes
         self.buffers = []
+        # 1: this population's launch starts each touched node's rhs/d from 0
+        # (it is the first to fold into them in a timestep); 0: accumulate
+        self.assign = 0
 
     def alloc(self, nbytes):
         b = rt.DeviceBuffer(nbytes)
@@ -179,13 +182,10 @@ class DeviceInstanceData:
         self.ptr = {name: self.arena.ptr + i * stride for i, name in enumerate(self.names)}
         self.ptr["i_acc"] = self.arena.ptr + len(self.names) * stride
         self.ptr["g_acc"] = self.arena.ptr + (len(self.names) + 1) * stride
-        nrw = max(1, len(runner.abi.rw_scalars))
-        self.scalars_rw = rt.DeviceBuffer(8 * nrw)
-        # deferred-instance list + ping-pong counters (CudaOptions.defer)
-        self.defer_list = rt.DeviceBuffer(4 * max(n, 1)) if runner.options.defer else None
-        self.defer_count = rt.DeviceBuffer(8) if runner.options.defer else None
-        if self.defer_count is not None:
-            rt.memset(self.defer_count.ptr, 0, 8, runner.stream)
+        # kernel-written GLOBALs: two buffers (read / write) swapped per step
+        # by the generated launch_steps; between calls buffer 0 is current
+        self.nrw = max(1, len(runner.abi.rw_scalars))
+        self.scalars_rw = rt.DeviceBuffer(16 * self.nrw)
         self.prebad: dict[str, int] = {}
         self.nodes: NodeBinding | None = None
         # arrays a launch (or the voltage gather) may have changed since the
@@ -399,14 +399,10 @@ class CudaRunner:
                 vals.append(newton_rec or None)
             elif role == "scalars_rw":
                 vals.append(dev.scalars_rw.ptr)
+            elif role == "scalars_rw_out":
+                vals.append(dev.scalars_rw.ptr + 8 * dev.nrw)
             elif role == "node":
                 vals.append((0 if f.ctype == "i64" else None) if nb is None else getattr(nb, f.key))
-            elif role == "defer":
-                if f.key == "defer_par":
-                    vals.append(0)
-                else:
-                    buf = getattr(dev, f.key, None)
-                    vals.append(buf.ptr if buf is not None else None)
         return self.Struct(*vals)
 
     def _sync_scalars_in(self, dev) -> None:
@@ -432,9 +428,7 @@ class CudaRunner:
             raise ValueError("step_nodes needs bind_nodes() first")
         md = self._struct(dev, newton_rec)
         dev.dirty |= self._writes[kernel_name]
-        if getattr(dev, "defer_count", None) is not None:
-            # an aborted launch can leave a count behind; start every call clean
-            rt.memset(dev.defer_count.ptr, 0, 8, self.stream)
+        rt.set_device(self.device)
         rc = self.entry[kernel_name](C.byref(md), int(steps), C.c_void_p(self.stream.handle), self.flags)
         rt.check(rc, f"launch {self.mb.symbol}_{kernel_name}")
 
@@ -473,6 +467,7 @@ class CudaRunner:
                             dev.newton_iters.append(int(raw[step, q]))
         key = st.err_key
         # pre-existing non-finite values in arrays this launch never rewrites
+        # (prebad holds caller-order instance indices, like the error keys)
         written = set(self.abi.kernels["step" if kernel_name == "step_nodes" else kernel_name]["stores"])
         order = self.abi.array_order
         kcode = {"initialize": 0, "state_update": 1, "current_update": 2}[parts[0]]
@@ -485,15 +480,17 @@ class CudaRunner:
             if host_data is not None:
                 self.to_host(dev, host_data, only_dirty=True)
             raise _interp_error(self._message(key, st, dev))
+        # a completed launch rewrote (or checked) every array it stores: a
+        # non-finite value seen at upload is gone from those
+        for name in written:
+            dev.prebad.pop(name, None)
 
     def _message(self, key, st, dev) -> str:
         kernel = _KNAME[(key >> 62) & 3]
         phase = (key >> 61) & 1
         ordinal = (key >> 48) & 0x1FFF
         kind = (key >> 46) & 3
-        inst = key & ((1 << 40) - 1)
-        if dev.nodes is not None:
-            inst = int(dev.nodes.perm_host[inst])
+        inst = key & ((1 << 40) - 1)  # caller order (node kernels map through perm)
         if phase == 1:
             name = self.abi.array_order[ordinal]
             return f"non-finite value in {name!r} at instance {inst} after kernel {kernel}"
@@ -640,10 +637,6 @@ class CudaRunner:
         dev.reorder(nb.perm, s)
         self._mark("bind:reorder")
         dev.nodes = nb
-        # prescan indices refer to instance order; remap to sorted positions
-        if dev.prebad:
-            rank = nb.host_array("rank", s)
-            dev.prebad = {k: int(rank[v]) for k, v in dev.prebad.items()}
         return nb
 
     def gather_voltage(self, dev: DeviceInstanceData) -> None:
@@ -669,6 +662,7 @@ class CudaRunner:
             raise ValueError("shared ion slots need identical instance order")
         dst.ptr[dst_slot] = src.ptr[src_slot]
         dst.shared_slots = getattr(dst, "shared_slots", set()) | {dst_slot}
+        dst.dirty.add(dst_slot)  # holds the producer's values now: download it
 
     def node_arrays(self, dev: DeviceInstanceData) -> dict:
         nb = dev.nodes
@@ -747,16 +741,19 @@ def simulate(layout, data, steps: int, jac_mode: str = "exact", on_step=None, ru
 
 
 def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, node_d=None,
-                   jac_mode: str = "exact", runner: CudaRunner | None = None, timings: dict | None = None):
+                   jac_mode: str = "exact", runner: CudaRunner | None = None, timings: dict | None = None,
+                   reset: bool = True):
     """node_index run of one mechanism population (builder extension).
 
     Per timestep: v_i = node_v[node_index[i]]; nrn_state; nrn_cur; then
-    node_rhs[k] -= sum_i i_acc[i] and node_d[k] += sum_i g_acc[i] over the
-    instances i of node k in ascending instance order (deterministic; the
-    oracle restatement is oracle/nodes_np.py).  Instances are initialised
-    with the gathered voltage.  Returns (data, node_rhs, node_d); `data` is
-    updated in place in instance order.  `timings` (optional dict) receives
-    wall-clock seconds per phase.
+    node_rhs[k] = 0 - sum_i i_acc[i] and node_d[k] = 0 + sum_i g_acc[i] over
+    the instances i of node k in ascending instance order (deterministic; the
+    oracle restatement is oracle/nodes_np.py): the node arrays are rebuilt
+    every step, as a cable solver's matrix is.  With ``reset=False`` they
+    start from node_rhs/node_d and accumulate across steps instead.
+    Instances are initialised with the gathered voltage.  Returns (data,
+    node_rhs, node_d); `data` is updated in place in instance order.
+    `timings` (optional dict) receives wall-clock seconds per phase.
     """
     import time
 
@@ -768,6 +765,8 @@ def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, 
     # the node layout (node_index upload, stable sort, segments, tiles) is
     # built on a second stream while the instance store uploads
     aux = runner.aux_stream()
+    if reset:  # nodes without instances hold 0; the others are assigned every step
+        node_rhs = node_d = None
     prep = runner.prepare_nodes(int(data.n), node_index, node_v, node_rhs, node_d, stream=aux)
     # v is never uploaded (every instance's voltage is its node's); i_acc /
     # g_acc are outputs only
@@ -775,12 +774,12 @@ def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, 
     t["upload"] = clock() - t0
     t0 = clock()
     nb = runner.bind_nodes(dev, node_index, prepared=prep)
+    nb.assign = 1 if reset else 0
     runner.gather_voltage(dev)
     if not np.isfinite(node_v).all():
         # a non-finite node voltage is a pre-existing non-finite v for the
         # first instance (in caller order) that reads it
-        first = int(np.flatnonzero(~np.isfinite(node_v[np.asarray(node_index)]))[0])
-        dev.prebad["v"] = int(nb.host_array("rank", runner.stream)[first])
+        dev.prebad["v"] = int(np.flatnonzero(~np.isfinite(node_v[np.asarray(node_index)]))[0])
     t["bind_nodes"] = clock() - t0
     try:
         t0 = clock()

@@ -64,6 +64,12 @@ _SIGS = {
     "nmodl_event_destroy": (C.c_int, [C.c_void_p]),
     "nmodl_event_record": (C.c_int, [C.c_void_p, C.c_void_p]),
     "nmodl_stream_wait_event": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "nmodl_event_record_external": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "nmodl_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "nmodl_nccl_init": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.c_int]),
+    "nmodl_nccl_destroy": (C.c_int, [C.c_void_p]),
+    "nmodl_nccl_allreduce_f64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_int, C.c_void_p]),
+    "nmodl_nccl_allgather_f64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
     "nmodl_combine_unique": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p,
                                        C.c_int, C.c_void_p]),
     "nmodl_event_sync": (C.c_int, [C.c_void_p]),
@@ -89,10 +95,8 @@ _SIGS = {
     "nmodl_permute_i32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
     "nmodl_gather_v": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
     "nmodl_selftest_exp": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
-    "nmodl_selftest_exp_table": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
     "nmodl_selftest_div_approx": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
     "nmodl_selftest_exp_smem": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
-    "nmodl_selftest_exp_estrin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
 }
 RUNTIME_SYMBOLS = tuple(_SIGS)
 
@@ -148,6 +152,19 @@ def require_device(dev: int | None = None) -> int:
     return cur.value
 
 
+def set_device(dev: int) -> None:
+    """Make `dev` current for this host thread (a runner re-selects its own
+    device before every launch / copy, so runners on several devices can
+    share one process)."""
+    check(lib().nmodl_set_device(int(dev)), "cudaSetDevice")
+
+
+def current_device() -> int:
+    cur = C.c_int(0)
+    check(lib().nmodl_get_device(C.byref(cur)), "cudaGetDevice")
+    return cur.value
+
+
 @functools.lru_cache(maxsize=None)
 def device_info(dev: int = 0) -> dict:
     sm, l2, mem, ma, mi = C.c_int(), C.c_longlong(), C.c_longlong(), C.c_int(), C.c_int()
@@ -158,7 +175,7 @@ def device_info(dev: int = 0) -> dict:
             "cc": (ma.value, mi.value), "name": name.value.decode()}
 
 
-_POOL: dict[int, list[int]] = {}
+_POOL: dict[tuple[int, int], list[int]] = {}  # (device, size) -> free blocks
 _POOL_BYTES = 0
 _POOL_CAP = 32 << 30  # keep at most 32 GiB of freed blocks for reuse
 _pool_lock = threading.Lock()
@@ -168,15 +185,19 @@ def empty_cache() -> None:
     """Return every cached free block to the driver."""
     global _POOL_BYTES
     with _pool_lock:
-        for size, ptrs in _POOL.items():
+        cur = current_device()
+        for (dev, _size), ptrs in _POOL.items():
+            set_device(dev)
             for p in ptrs:
                 lib().nmodl_free(C.c_void_p(p))
+        set_device(cur)
         _POOL.clear()
         _POOL_BYTES = 0
 
 
 class DeviceBuffer:
-    """Owned device allocation, recycled through a size-keyed cache.
+    """Owned device allocation on the current device, recycled through a
+    (device, size)-keyed cache.
 
     cudaMalloc/cudaFree of multi-GB SoA arenas synchronise the device and
     cost milliseconds each; a store that is uploaded, stepped and downloaded
@@ -185,19 +206,22 @@ class DeviceBuffer:
     def __init__(self, nbytes: int):
         global _POOL_BYTES
         self.nbytes = int(max(nbytes, 1))
-        key = (self.nbytes + 255) // 256 * 256
+        size = (self.nbytes + 255) // 256 * 256
+        self.device = current_device()
+        key = (self.device, size)
         self._key = key
+        self._size = size
         with _pool_lock:
             free = _POOL.get(key)
             if free:
                 self.ptr = free.pop()
-                _POOL_BYTES -= key
+                _POOL_BYTES -= size
                 return
         p = C.c_void_p()
-        rc = lib().nmodl_malloc(C.byref(p), key)
+        rc = lib().nmodl_malloc(C.byref(p), size)
         if rc != 0:  # out of memory: drop the cache and retry once
             empty_cache()
-            rc = lib().nmodl_malloc(C.byref(p), key)
+            rc = lib().nmodl_malloc(C.byref(p), size)
         check(rc, f"cudaMalloc({nbytes})")
         self.ptr = p.value
 
@@ -205,12 +229,12 @@ class DeviceBuffer:
         global _POOL_BYTES
         if self.ptr:
             with _pool_lock:
-                if _POOL_BYTES + self._key <= _POOL_CAP:
+                if _POOL_BYTES + self._size <= _POOL_CAP:
                     _POOL.setdefault(self._key, []).append(self.ptr)
-                    _POOL_BYTES += self._key
+                    _POOL_BYTES += self._size
                     self.ptr = None
                     return
-            lib().nmodl_free(C.c_void_p(self.ptr))
+            lib().nmodl_free(C.c_void_p(self.ptr))  # cudaFree needs no current-device match
             self.ptr = None
 
     def __del__(self):
@@ -249,6 +273,11 @@ class Event:
 
     def record(self, stream: Stream) -> None:
         check(lib().nmodl_event_record(C.c_void_p(self.handle), C.c_void_p(stream.handle)), "event_record")
+
+    def record_external(self, stream: Stream) -> None:
+        """Timestamped even inside a graph capture (kernel boundaries of a replay)."""
+        check(lib().nmodl_event_record_external(C.c_void_p(self.handle), C.c_void_p(stream.handle)),
+              "event_record_external")
 
     def sync(self) -> None:
         check(lib().nmodl_event_sync(C.c_void_p(self.handle)), "event_sync")

@@ -6,21 +6,36 @@ RELAXED = [dict(recip=True), dict(div_approx=True), dict(recip=True, div_approx=
            dict(exp_smem=True, pipe=True, grid_waves=0),
            dict(recip=True, div_approx=True, pipe=True, fast_redo=True, ilp=2),
            dict(recip=True, quot=True, div_approx=True, exp_share=True, pipe=True, fast_redo=True),
-           dict(recip=True, quot=True, exp_share=True, exp_smem=True, fast_path=False),
-           dict(exp_estrin=True, fast_path=False)]
+           dict(recip=True, quot=True, exp_share=True, exp_smem=True, fast_path=False)]
 RELAXED_STEMS = ["hh_subset", "NaTs2_t", "Ca_HVA", "Ih", "na6", "cdp5ish", "ProbAMPANMDA_EMS",
                  "corpus_cat", "corpus_vtrap", "corpus_kdr", "K_Pst", "SKv3_1"]
 PIPE_STEMS = ["hh_subset", "NaTs2_t", "na6", "cdp5ish", "ProbAMPANMDA_EMS", "corpus_cat", "cadyn"]
 WAVES_STEMS = ["hh_subset", "NaTs2_t", "cdp5ish", "ProbAMPANMDA_EMS"]
-DEFER_STEMS = ["hh_subset", "NaTs2_t", "na6", "cdp5ish", "ProbAMPANMDA_EMS", "corpus_cat"]
+
+
+# the fast-path fallback test also runs bench.py's own builds of these stems
+FALLBACK_BENCH_STEMS = ["hh_subset", "NaTs2_t", "K_Pst"]
+
+
+def _bench_builds():
+    import dataclasses
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    from bench import options_for
+
+    return [(st, {f.name: getattr(options_for(st), f.name) for f in dataclasses.fields(options_for(st))})
+            for st in FALLBACK_BENCH_STEMS]
+
+
+FALLBACK_BENCH = _bench_builds()
 
 
 def variants():
     out = []
     for st in ("hh_subset", "ProbAMPANMDA_EMS"):
         out.append((st, dict(ilp=2)))
-    for st in DEFER_STEMS:
-        out.append((st, dict(fast_path=True, defer=True)))
     for st in PIPE_STEMS:
         for ilp in (1, 2):
             out.append((st, dict(ilp=ilp, pipe=True)))
@@ -30,13 +45,9 @@ def variants():
     for w, t in ((0, 2048), (0, 256), (2, 1024)):
         out.append(("ProbAMPANMDA_EMS", dict(fast_path=False, tile=t, grid_waves=w)))
     for t in (512, 128, 64, 2048):
-        for kw in (dict(fast_path=False, pipe=True), dict(fast_path=True, fast_redo=True, pipe=True),
-                   dict(fast_path=False, warp_tiles=True), dict(fast_path=True, fast_redo=True, idx_ahead=True)):
-            out.append(("ProbAMPANMDA_EMS", dict(tile=min(t, 256) if kw.get("warp_tiles") else t, **kw)))
+        for kw in (dict(fast_path=False, pipe=True), dict(fast_path=True, fast_redo=True, pipe=True)):
+            out.append(("ProbAMPANMDA_EMS", dict(tile=t, **kw)))
     out.append(("ProbAMPANMDA_EMS", dict(fast_path=False, pipe=True)))
-    out.append(("ProbAMPANMDA_EMS", dict(fast_path=False, warp_tiles=True, tile=256)))
-    for t in (512, 256, 128):
-        out.append(("ProbAMPANMDA_EMS", dict(bulk=True, tile=t, fast_path=False)))
     for st in ("hh_subset", "NaTs2_t", "corpus_cat", "cdp5ish"):
         for kw in (dict(fast_redo=True), dict(fast_redo=True, pipe=True), dict(fast_redo=True, pipe=True, ilp=2),
                    dict(fast_redo=True, pipe=True, recip=True, div_approx=True, exp_smem=True)):
@@ -46,9 +57,8 @@ def variants():
         out.append((st, dict(lu_spec=True, fast_path=True, fast_redo=True, pipe=True)))
     for st in ("hh_subset", "ProbAMPANMDA_EMS", "corpus_exp2syn"):
         out.append((st, dict(fmad=True)))
-    for st in ("hh_subset", "NaTs2_t", "K_Pst", "ProbAMPANMDA_EMS", "na6", "corpus_cat"):
-        for fast in (False, True):
-            out.append((st, dict(exp_table=True, fast_path=fast)))
+    for st, kw in FALLBACK_BENCH:
+        out.append((st, kw))
     for st in RELAXED_STEMS:
         for r in RELAXED:
             out.append((st, {"fast_path": True, **r}))

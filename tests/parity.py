@@ -5,6 +5,7 @@ from paper_1905_02241_b200.metrics import (  # noqa: F401
     compared_names,
     g_acc_dev,
     group_dev,
+    node_dev,
     parity,
     rel_dev,
     rel_dev_floor,

@@ -7,7 +7,7 @@ import pytest
 
 from oracle import column_np as CN
 from oracle import interp_np as O
-from parity import TOL, parity
+from parity import TOL, node_dev, parity
 
 pytestmark = pytest.mark.gpu
 
@@ -36,17 +36,16 @@ def test_small_column_matches_oracle(bench_options, concurrent):
     datas = {m: init_range(irs[m], lay["mechs"][m][0], lay["mechs"][m][1], spec.seed) for m in LAUNCH_ORDER}
     datas = {m: O.InstanceData(x.n, x.arrays, x.acc, x.scalars) for m, x in datas.items()}
     idx = {m: lay["mechs"][m][2] for m in LAUNCH_ORDER}
-    ref, rhs, d = CN.simulate_column(irs, datas, idx, lay["node_v"], LAUNCH_ORDER, COUPLINGS, steps)
+    terms = {}
+    ref, rhs, d = CN.simulate_column(irs, datas, idx, lay["node_v"], LAUNCH_ORDER, COUPLINGS, steps, terms=terms)
     for m in LAUNCH_ORDER:
         got = init_range(irs[m], lay["mechs"][m][0], lay["mechs"][m][1], spec.seed)
         shard.runners[m].to_host(shard.devs[m], got)
         dev, where = parity(irs[m], ref[m], got)
         assert dev <= TOL, (m, dev, where)
     nodes = shard.nodes.download(shard.stream)
-    for name, want in (("node_rhs", rhs), ("node_d", d)):
-        got = nodes[name]
-        den = np.maximum(np.maximum(np.abs(got), np.abs(want)), 1e-30)
-        assert np.max(np.abs(got - want) / den) <= 1e-9, name
+    for name, want, scale in (("node_rhs", rhs, terms["rhs"]), ("node_d", d, terms["d"])):
+        assert node_dev(nodes[name], want, scale) <= 1e-10, name
 
 
 def test_column_shards_add_up():
@@ -84,3 +83,40 @@ def test_concurrent_soma_is_bit_identical_and_graph_capturable():
         np.testing.assert_array_equal(a[k].view(np.int64), b[k].view(np.int64), err_msg=k)
     np.testing.assert_array_equal(seq.checksums(), con.checksums())
     assert set(LAUNCH_ORDER)
+
+
+def test_two_process_column_shards(tmp_path):
+    """Two real processes, each owning a CudaRunner shard of the column's cells
+    (parallel.partition_cells), all-gather their device checksums through the
+    product's process group (ranks sharing this one GPU -> FileGroup; NCCL
+    needs a GPU per rank).  The gathered table equals, bit for bit, the
+    tables of the same two shards built in this process, and the shards add
+    up to the whole column."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    from paper_1905_02241_b200.column import ColumnShard, ColumnSpec
+
+    n_cells, steps, world = 500, 20, 2
+    out = str(tmp_path / "table.npy")
+    worker = Path(__file__).resolve().parent / "mp_column_worker.py"
+    procs = []
+    for r in range(world):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), LOCAL_RANK=str(r),
+                   NMODL_BOOTSTRAP_DIR=str(tmp_path / "boot"))
+        procs.append(subprocess.Popen([sys.executable, str(worker), out, str(n_cells), str(steps)], env=env))
+    for p in procs:
+        assert p.wait(timeout=600) == 0
+    table = np.load(out)
+    bounds = np.load(out + ".bounds.npy")
+    spec = ColumnSpec(n_cells=n_cells, dend_per_cell=4, syn_per_cell=10, seed=3)
+    for r in range(world):
+        s = ColumnShard(spec, int(bounds[r]), int(bounds[r + 1]))
+        s.launch(steps)
+        s.check()
+        np.testing.assert_array_equal(table[r], s.checksums())
+    whole = ColumnShard(spec, 0, n_cells)
+    whole.launch(steps)
+    np.testing.assert_allclose(table[0][:, 1] + table[1][:, 1], whole.checksums()[:, 1], rtol=1e-12)

@@ -7,13 +7,17 @@ domain gives exact size-independent checks:
   instances of an n-instance store equal a k-instance store, and instances
   never interact (modlc/interp.py:55-84, 706-723): the first 65,536 results
   of the full-size GPU run must match the oracle run on 65,536 instances;
-* node sums -- node rhs/d at full size must be bit-identical to sequential
-  np.subtract.at / np.add.at applied to the GPU's own per-instance currents;
+* node sums -- node rhs/d are rebuilt every step, so after the full-size
+  run they must be bit-identical to sequential np.subtract.at / np.add.at
+  applied to the GPU's own final per-instance currents;
 * determinism / permutation invariance -- two full-size runs, one of them on
   a permuted store, give bit-identical per-instance results.
 
-The full-size runs use the builds bench.py measures (bench.options_for);
-the default builds are covered at small sizes by test_gpu_parity.py.
+The full-size runs use the builds bench.py measures (bench.options_for) and
+its population set-up (bbp20m's Ca_HVA -> CaDynamics_E2 shared ica slot);
+the oracle side of the 65,536-instance prefixes runs chunked over the host
+cores (tests/oracle_pool.py).  The default builds are covered at small sizes
+by test_gpu_parity.py.
 """
 
 import numpy as np
@@ -22,6 +26,7 @@ import pytest
 from conftest import load_ir
 from oracle import interp_np as O
 from oracle import nodes_np as N
+from oracle_pool import oracle_prefix
 from parity import TOL, parity
 
 pytestmark = pytest.mark.gpu
@@ -65,36 +70,62 @@ def test_synapse_10m_nodes_1000_steps():
     ref, _, _ = N.simulate_nodes(ir, ref, steps, idx[:PREFIX], nv)
     dev, where = parity(ir, ref, _prefix(gpu, PREFIX))
     assert dev <= TOL, (dev, where)
-    # the last step's node reduction is bit-exact given the per-instance currents:
-    # replay all steps' scatters is not possible (only the final currents are
-    # kept), so check one fresh step from the final state
-    runner = CudaRunner(ir)
-    dev_store = runner.to_device(gpu)
-    nb = runner.bind_nodes(dev_store, idx, nv)
-    runner.run_kernel(dev_store, "step_nodes", 1)
-    after = init(ir, n, 0)
-    runner.to_host(dev_store, after)
-    got = runner.node_arrays(dev_store)
+    # node rhs/d hold the last step's reduction (per-step reset): bit-exact
+    # against the in-order scatter of the GPU's own final currents
     rhs_ref, d_ref = np.zeros(n_nodes), np.zeros(n_nodes)
-    N.scatter(rhs_ref, d_ref, idx, after.acc["i_acc"], after.acc["g_acc"])
-    np.testing.assert_array_equal(got["node_rhs"], rhs_ref)
-    np.testing.assert_array_equal(got["node_d"], d_ref)
+    N.scatter(rhs_ref, d_ref, idx, gpu.acc["i_acc"], gpu.acc["g_acc"])
+    np.testing.assert_array_equal(rhs, rhs_ref)
+    np.testing.assert_array_equal(d, d_ref)
     assert np.all(np.isfinite(rhs)) and np.all(np.isfinite(d))
 
 
-def test_bbp_set_prefix_and_permutation_invariance():
+def test_bbp20m_coupled_as_bench_runs_it():
+    """bench.py's bbp20m step exactly: six populations of 3,333,333 instances,
+    its builds, one stream in launch order, CaDynamics_E2 reading Ca_HVA's ica
+    array (share_slot), nrn_init then 1000 steps; the first 65,536 instances
+    of every population vs the coupled oracle (same order, same coupling)."""
+    from bench import WORKLOADS
+    from paper_1905_02241_b200.instance import init
+
+    w = WORKLOADS["bbp20m"]
+    stems = [m for m, _ in w["mechs"]]
+    n, steps = w["mechs"][0][1], 1000
+    runners, devs = {}, {}
+    for m in stems:
+        ir = load_ir(m)
+        r = _runner(m, ir)
+        devs[m] = r.to_device(init(ir, n, 42))
+        r.run_kernel(devs[m], "initialize", 1)
+        runners[m] = r
+    for dst, dslot, src, sslot in w["couplings"]:
+        runners[dst].share_slot(devs[dst], dslot, devs[src], sslot)
+    s0 = runners[stems[0]].stream
+    for m in stems:
+        runners[m].stream = s0
+    for _ in range(steps):
+        for m in stems:
+            runners[m].launch(devs[m], "step", 1)
+    s0.sync()
+    ref = oracle_prefix(stems, PREFIX, steps, 42, w["couplings"])
+    for m in stems:
+        runners[m].check(devs[m])
+        got = init(load_ir(m), n, 0)
+        runners[m].to_host(devs[m], got)
+        dev, where = parity(load_ir(m), ref[m], _prefix(got, PREFIX))
+        assert dev <= TOL, (m, dev, where)
+        del got
+
+
+def test_bbp_set_permutation_invariance():
     from paper_1905_02241_b200.instance import init
     from paper_1905_02241_b200.runner import CudaRunner, simulate
 
-    n, steps = 3_333_333, 1000
+    n, steps = 3_333_333, 300
     for stem in ("NaTs2_t", "K_Pst", "Ca_HVA", "SKv3_1", "Ih", "cadyn"):
         ir = load_ir(stem)
         runner = _runner(stem, ir)
         base = init(ir, n, 42)
         gpu = simulate(ir, base.copy(), steps, runner=runner)
-        ref = O.simulate(ir, O.init(ir, 8192, 42), steps)
-        dev, where = parity(ir, ref, _prefix(gpu, 8192))
-        assert dev <= TOL, (stem, dev, where)
         # permuted store -> identical per-instance bits after un-permuting
         perm = np.random.default_rng(1).permutation(n)
         shuffled = base.copy()
@@ -113,8 +144,8 @@ def test_kinetic_1m_prefix():
     for stem in ("na6", "cdp5ish"):
         ir = load_ir(stem)
         gpu = simulate(ir, init(ir, 1_000_000, 42), 1000, runner=_runner(stem, ir))
-        ref = O.simulate(ir, O.init(ir, 4096, 42), 1000)
-        dev, where = parity(ir, ref, _prefix(gpu, 4096))
+        ref = oracle_prefix([stem], PREFIX, 1000, 42)[stem]
+        dev, where = parity(ir, ref, _prefix(gpu, PREFIX))
         assert dev <= TOL, (stem, dev, where)
         if stem == "cdp5ish":
             assert gpu.newton_iters and max(gpu.newton_iters) <= 50

@@ -290,8 +290,7 @@ OPTION_SETS = [
     ("K_Pst", dict(ilp=2, recip=True, quot=True, exp_smem=True, pipe=True, fast_path=True, fast_redo=True)),
     ("na6", dict(lu_spec=True, pipe=True, fast_path=True, fast_redo=True)),
     ("cdp5ish", dict(lu_spec=True, div_approx=True, fast_path=True)),
-    ("ProbAMPANMDA_EMS", dict(warp_tiles=True, tile=256, fast_path=False)),
-    ("ProbAMPANMDA_EMS", dict(idx_ahead=True, fast_path=False)),
+    ("ProbAMPANMDA_EMS", dict(ilp=2, fast_path=False)),
     ("ProbAMPANMDA_EMS", dict(pipe=True, fast_path=True, fast_redo=True, grid_waves=0)),
 ]
 
@@ -384,3 +383,25 @@ def test_census_next_to_measured_ncu_counters():
     assert 0 < r["hbm_fraction_algorithmic"] <= 1 and 0 < r["fp64_pipe_fraction"] <= 1
     assert r["measured_fp64_instr"] < r["census_fp64_ops"]  # relaxed build: fewer than the census prices
     assert 80 < r["measured_dram_bytes"] < 150
+
+
+def test_codegen_hazards_rwglobal():
+    """Text-level guards for two code-generation hazards (fixtures/mod/rwglobal.mod):
+    kernel-written GLOBALs are read from one buffer and written to the other
+    (no in-launch read-after-write between instance 0 and later blocks), the
+    v+h pass's GLOBAL write is carried into the base pass, and an exp of a
+    slot is recomputed after the slot is reassigned (exp_share)."""
+    import re
+
+    from paper_1905_02241_b200.codegen_cuda import CudaOptions, emit_cuda
+
+    ir = load_ir("rwglobal")
+    text = emit_cuda(ir, CudaOptions(exp_share=True, fast_redo=True, pipe=True)).text
+    assert "md.scalars_rw_out[0] = " in text
+    assert not re.search(r"md\.scalars_rw\[\d+\] =", text)
+    assert "local.scalars_rw_out = md->scalars_rw + ((step + 1) & 1) * 1;" in text
+    assert "I.g_cnt = S.g_cnt;" in text
+    body = text[text.index("rwglobal_body_state_update"):text.index("rwglobal_body_current_update")]
+    first, second = body.index("I.s = I.v;"), body.rindex("NM_EXP")
+    exps_of_s = re.findall(r"const double (t_xs\d+) = NM_EXP\(\(double\)\(\(rwglobal_K\[\d+\] \* I\.s\)\)\);", body)
+    assert len(exps_of_s) == 2 and first < second

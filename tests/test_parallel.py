@@ -1,8 +1,11 @@
-"""Multi-process (world_size 2, gloo on CPU) coverage of the sharding path.
+"""Multi-process (world_size 2, CPU) coverage of the sharding path.
 
 The GPU hot path has no per-step collective; what crosses ranks is (1) the
 cell partition every rank computes identically and (2) the end-of-run
-checksum all-gather.  Both are exercised here with two real processes.
+checksum all-gather.  Both are exercised here with two real processes
+through the product's torch-free FileGroup (parallel.py), and the same
+all-gather is cross-checked against torch.distributed's gloo backend (test
+only: the product never imports torch).
 """
 
 import os
@@ -12,7 +15,8 @@ import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
-from paper_1905_02241_b200.parallel import gather_checksums, host_checksums, partition_cells, shard_instances
+from paper_1905_02241_b200.parallel import (FileGroup, gather_checksums, host_checksums, init_group,
+                                            partition_cells, shard_instances)
 
 
 def test_partition_balances_cost_and_covers_all_cells():
@@ -47,12 +51,13 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, boot):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    group = FileGroup(boot, rank, world)
     try:
         from conftest import load_ir
         from oracle import interp_np as O
@@ -68,13 +73,22 @@ def _worker(rank, world, port, q):
         O.simulate(ir, shard, 5)
         names = list(ir.slot_names())
         local = host_checksums(shard.arrays, names)
-        table = gather_checksums(local)
+        table = gather_checksums(local, group)
+        # cross-check: gloo's all_gather delivers the same table
+        import torch
+
+        parts = [torch.empty(local.shape, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.as_tensor(local))
+        assert np.array_equal(np.stack([p.numpy() for p in parts]), table)
+        assert group.allreduce([float(rank + 1)], "max") == [float(world)]
+        assert group.allreduce([1.0, 2.0], "sum") == [float(world), 2.0 * world]
         q.put((rank, table.tolist(), (lo, hi)))
     finally:
+        group.close()
         dist.destroy_process_group()
 
 
-def test_two_rank_shards_reassemble_to_single_run():
+def test_two_rank_shards_reassemble_to_single_run(tmp_path):
     import sys
     from pathlib import Path
 
@@ -83,7 +97,7 @@ def test_two_rank_shards_reassemble_to_single_run():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, str(tmp_path / "grp"))) for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=120) for _ in range(world)]
@@ -105,3 +119,34 @@ def test_two_rank_shards_reassemble_to_single_run():
         a = full.arrays[name]
         assert np.isclose(t0[0][name_i][0] + t0[1][name_i][0], a[lo0:hi0].sum() + a[lo1:hi1].sum(), rtol=1e-12)
         assert hi0 == lo1
+
+
+def test_init_group_single_rank_and_file_fallback(monkeypatch, tmp_path):
+    """WORLD_SIZE=1 -> LocalGroup; more ranks than GPUs -> FileGroup (ranks
+    sharing a device; NCCL needs one GPU per rank)."""
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    g, dev = init_group(device_count=0)
+    assert g.world == 1 and g.backend == "local" and dev == 0
+    assert gather_checksums(np.ones((2, 2)), g).shape == (1, 2, 2)
+    monkeypatch.setenv("WORLD_SIZE", "1")
+    monkeypatch.setenv("NMODL_BOOTSTRAP_DIR", str(tmp_path))
+    g, _ = init_group(device_count=1)
+    assert g.backend == "local"
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    monkeypatch.setenv("RANK", "1")
+    monkeypatch.setenv("LOCAL_RANK", "1")
+    g, dev = init_group(device_count=1)
+    assert g.backend == "file" and g.rank == 1 and dev == 0
+
+
+def test_product_modules_do_not_import_torch():
+    """The package and bench.py's product arm run without PyTorch."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    code = ("import sys; sys.path.insert(0, %r); import paper_1905_02241_b200, paper_1905_02241_b200.parallel, "
+            "paper_1905_02241_b200.runner, paper_1905_02241_b200.column, bench; "
+            "assert 'torch' not in sys.modules, 'torch imported'" % str(root))
+    subprocess.run([sys.executable, "-c", code], check=True, timeout=300)

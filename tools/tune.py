@@ -8,6 +8,7 @@ algorithmic GB/s and instance-steps/s.  Used to pick bench.py's options.
 """
 
 import json
+import os
 import sys
 import time
 from pathlib import Path
@@ -33,7 +34,7 @@ VARIANTS = [CudaOptions(**a, **b) for b in CODEGEN for a in SHAPES]
 
 def run(stem, opts, nodes=0, steps=30):
     ir = MechIR.load(ROOT / "fixtures" / "ir" / f"{stem}.json")
-    n = SIZES.get(stem, 1_000_000)
+    n = int(os.environ.get("TUNE_N", SIZES.get(stem, 1_000_000)))
     r = CudaRunner(ir, options=opts)
     dev = r.to_device(init(ir, n, 42))
     kernel = "step"
@@ -46,8 +47,6 @@ def run(stem, opts, nodes=0, steps=30):
     lb = launch_bytes(r.abi, n, kernel, nodes)
     flush = rt.DeviceBuffer(2 * info["l2_bytes"]) if lb < 3 * info["l2_bytes"] else None
     a, b = rt.Event(), rt.Event()
-    import os
-
     for _ in range(int(os.environ.get("TUNE_WARMUP", "10"))):
         r.launch(dev, kernel, 1)
     r.stream.sync()
@@ -68,6 +67,9 @@ def run(stem, opts, nodes=0, steps=30):
             "ms": ms, "GBps": lb / (ms / 1e3) / 1e9, "inst_steps_per_s": n / (ms / 1e3), "flush": bool(flush)}
 
 
+BOOL_OPTS = tuple(f.name for f in __import__("dataclasses").fields(CudaOptions) if f.type in (bool, "bool"))
+
+
 def grid(spec: str):
     """'ilp=1,2 fast_path=0,1' -> the CudaOptions cross product."""
     import itertools
@@ -76,7 +78,7 @@ def grid(spec: str):
     for part in spec.split():
         k, vs = part.split("=")
         keys.append(k)
-        values.append([bool(int(v)) if k in ("fast_path", "exp_c", "const_pool", "fast_div", "const_div", "exp_inline", "stream_hints", "fmad", "bulk", "defer", "exp_table", "pipe", "recip", "div_approx", "exp_smem", "fast_redo", "lu_spec", "warp_tiles", "idx_ahead", "quot", "exp_estrin", "exp_share") else int(v)
+        values.append([bool(int(v)) if k in BOOL_OPTS else int(v)
                        for v in vs.split(",")])
     return [CudaOptions(**dict(zip(keys, combo))) for combo in itertools.product(*values)]
 

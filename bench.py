@@ -1,11 +1,12 @@
 """Benchmark: nrn_state + nrn_cur instance-steps/s (fp64) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload synapse10m|hh1m|bbp20m|kinetic1m] [--no-also]
+                    [--workload synapse10m|hh1m|hh10m|bbp20m|kinetic1m|column]
+                    [--no-also] [--no-e2e] [--no-cpu] [--no-sustained]
 
 One JSON line on rank 0.  A "step" is one timestep of the hot path over the
 whole synthetic population on every rank: one fused nrn_state+nrn_cur launch
-per mechanism (for the default workload also the node_index gather and the
+per mechanism (for node_index workloads also the voltage gather and the
 in-order rhs/d reduction, inside the same kernel).  Workloads are the
 BASELINE.json configs:
 
@@ -14,17 +15,27 @@ BASELINE.json configs:
                           node_index onto 1M nodes (default; inputs >> L2)
   hh1m        configs[0]  hh (cnexp, analytic conductance), 1M instances / GPU
                           (working set ~ L2: L2 flushed between timed steps)
+  hh10m       configs[0]'s mechanism at 10M instances (inputs >> L2): the
+                          same kernel where the 1M size floor does not bind
   bbp20m      configs[2]  NaTs2_t, K_Pst, Ca_HVA, SKv3_1, Ih, CaDynamics_E2;
                           20M instances / GPU split evenly (6 launches / step)
   kinetic1m   configs[3]  6-state KINETIC Na (runtime LU k=6) + cdp5-style
                           Newton k=5 with LU, 1M instances each
+  column      configs[4]  100k-cell synthetic column, cells split over ranks
+                          (strong scaling)
 
+Timing: W untimed warm-up steps, then K steps replayed from one CUDA graph
+bracketed by a barrier and a synchronize on both sides; CUDA events recorded
+INSIDE the graph (external event-record nodes) around every population's
+launch give each kernel's launch duration within the same timed replay.
 Multi-GPU (torchrun): one process per GPU, each rank owns its own shard of
-cells (weak scaling, no per-step collective); timings are CUDA events on the
-launching stream, max over ranks; NCCL only all-reduces validation checksums.
-`--impl reference` times the reference's own CPU implementation (its emitted
-scalar C, oracle/_ref, compiled -O3 -march=native, all host threads) on a
-bounded sample of the same workload, rank 0 only.
+cells, max-over-ranks time; collectives (barrier, max time, checksum
+all-gather) go through paper_1905_02241_b200.parallel (NCCL bound by the
+runtime library; no PyTorch anywhere).  `--impl reference` times the
+reference's own CPU implementation (its emitted scalar C, oracle/_ref,
+compiled -O3 -march=native, all host threads) on a bounded sample of the
+same workload, rank 0 only; the ours-arm `cpu_baseline` is the same
+measurement with a smaller step count.
 """
 
 from __future__ import annotations
@@ -55,6 +66,8 @@ WORKLOADS = {
         "nodes": 1_000_000,
     },
     "hh1m": {"config": BASELINE["configs"][0], "mechs": [("hh_subset", 1_000_000)], "nodes": 0},
+    "hh10m": {"config": BASELINE["configs"][0] + " -- at 10M instances (inputs >> L2)",
+              "mechs": [("hh_subset", 10_000_000)], "nodes": 0},
     "bbp20m": {
         "config": BASELINE["configs"][2],
         "mechs": [(m, 20_000_000 // 6) for m in ("NaTs2_t", "K_Pst", "Ca_HVA", "SKv3_1", "Ih", "cadyn")],
@@ -188,57 +201,47 @@ class ClockSampler:
 
 
 class Dist:
-    """torchrun plumbing: one process per GPU; NCCL for the (tiny) barrier /
-    max-time / checksum collectives.  When fewer GPUs than ranks are visible
-    (a multi-rank smoke test on one GPU) ranks share devices and the
-    collectives fall back to gloo."""
+    """One process per GPU (torchrun env: RANK / WORLD_SIZE / LOCAL_RANK).
+    The process group is paper_1905_02241_b200.parallel.init_group: NCCL
+    through the runtime library when every rank has its own GPU, a file
+    group when ranks share one (a multi-rank smoke run on a one-GPU box),
+    the identity for one rank.  No PyTorch."""
 
-    def __init__(self):
+    def __init__(self, need_group: bool = True):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
-        self.local = int(os.environ.get("LOCAL_RANK", "0"))
-        self.device = self.local
-        self.pg = None
-        self.backend = None
-        if self.world > 1 or os.environ.get("TORCHELASTIC_RUN_ID"):
-            import torch
-            import torch.distributed as dist
+        self.device = 0
+        self.group = None
+        if need_group:
+            from paper_1905_02241_b200.parallel import init_group
 
-            ndev = max(torch.cuda.device_count(), 1)
-            self.device = self.local % ndev
-            torch.cuda.set_device(self.device)
-            if ndev >= self.world:
-                self.backend = "nccl"
-                dist.init_process_group("nccl", device_id=torch.device("cuda", self.device))
-            else:
-                self.backend = "gloo"
-                dist.init_process_group("gloo")
-            self.pg = dist
+            self.group, self.device = init_group()
 
     @property
-    def tensor_device(self):
-        return f"cuda:{self.device}" if self.backend == "nccl" else None
+    def backend(self):
+        return getattr(self.group, "backend", "none")
 
     def barrier(self):
-        if self.pg:
-            self.pg.barrier()
+        if self.group is not None:
+            self.group.barrier()
 
     def allreduce(self, values, op="max"):
-        if not self.pg:
-            return list(values)
-        import torch
+        if self.group is None:
+            return [float(v) for v in values]
+        return self.group.allreduce(values, op)
 
-        t = torch.tensor(list(values), dtype=torch.float64, device=self.tensor_device or "cpu")
-        self.pg.all_reduce(t, op={"max": self.pg.ReduceOp.MAX, "sum": self.pg.ReduceOp.SUM}[op])
-        return t.cpu().tolist()
+    def allgather(self, local):
+        from paper_1905_02241_b200.parallel import gather_checksums
+
+        return gather_checksums(local, self.group)
 
     def close(self):
-        if self.pg:
-            self.pg.destroy_process_group()
+        if self.group is not None:
+            self.group.close()
 
 
 # ---------------------------------------------------------------------------
-# our implementation
+# roofline denominators and the ncu traffic record
 
 
 def _peaks():
@@ -249,12 +252,80 @@ def _peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def _ncu_traffic(workload):
-    p = ROOT / "profiles" / "ncu_traffic.json"
+def _fp64_peak(sm_mhz=None):
+    """FP64 pipe instructions/s: the DFMA microbenchmark's measured rate
+    (tools/micro/fp64_peak.cu -> profiles/fp64_peak.json), else 148 SMs x 64
+    lanes x the sampled SM clock."""
+    p = ROOT / "profiles" / "fp64_peak.json"
     if p.is_file():
         d = json.loads(p.read_text())
-        return d.get(workload)
-    return None
+        return float(d["dfma_per_s"]), f"measured ({d.get('source', 'profiles/fp64_peak.json')})"
+    mhz = sm_mhz or 1965.0
+    return 148 * 64 * mhz * 1e6, f"nominal 148 SM x 64 FP64 lanes x {mhz:.0f} MHz"
+
+
+def _traffic_record():
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    return json.loads(p.read_text()) if p.is_file() else {}
+
+
+def _traffic(build_keys):
+    """ncu DRAM bytes (read + write) per launch of these exact builds (the
+    content-addressed library stem: generated text + flags + headers), from
+    `ncu --set full` captures of the same bench configuration
+    (tools/profile_bench.py); None unless every build was captured."""
+    rec = _traffic_record().get("by_build", {})
+    total = 0.0
+    for k in build_keys:
+        e = rec.get(k)
+        if e is None:
+            return None, f"no ncu capture of build {k}"
+        total += e["dram_bytes"]
+    return total, "ncu --set full capture of the same build(s): " + ", ".join(
+        rec[k].get("capture", "?") for k in build_keys)
+
+
+def _fp64_ops(ir):
+    from paper_1905_02241_b200.analysis import fp64_ops
+
+    return fp64_ops(ir)
+
+
+def _roofline(kernel_name, bytes_per_launch, fp64_per_launch, launch_ms, build_keys, sm_mhz):
+    """roofline object of one kernel launch: algorithmic bytes (and census FP64
+    pipe instructions) of one launch / its measured duration, against the
+    measured HBM copy peak (and the measured DFMA rate).  `bound` is the
+    static classification: the roof the kernel would reach first."""
+    peak, peak_src = _peaks()
+    fpeak, fpeak_src = _fp64_peak(sm_mhz)
+    s = launch_ms / 1e3
+    achieved = bytes_per_launch / s / 1e9
+    t_hbm = bytes_per_launch / (peak * 1e9)
+    t_fp = fp64_per_launch / fpeak
+    traffic, tnote = _traffic(build_keys)
+    return {
+        "bound": "hbm" if t_hbm >= t_fp else "fp64",
+        "kernel": kernel_name,
+        "achieved": achieved,
+        "peak": peak,
+        "unit": "GB/s",
+        "frac": achieved / peak,
+        "traffic": traffic,
+        "traffic_source": tnote,
+        "peak_source": peak_src,
+        "bytes_per_launch": bytes_per_launch,
+        "launch_ms": launch_ms,
+        "fp64": {"achieved": fp64_per_launch / s / 1e9, "peak": fpeak / 1e9, "unit": "G FP64-pipe instr/s",
+                 "frac": fp64_per_launch / s / fpeak, "instr_per_launch": fp64_per_launch,
+                 "peak_source": fpeak_src,
+                 "model": "census of the fused nrn_state+nrn_cur (analysis.fp64_ops: reference census priced "
+                          "with the emitted instruction sequences)"},
+        "max_hbm_frac_at_fp64_roof": min(1.0, t_hbm / t_fp) if t_fp > 0 else 1.0,
+    }
+
+
+# ---------------------------------------------------------------------------
+# our implementation
 
 
 class Population:
@@ -270,24 +341,25 @@ class Population:
         self.n = n
         self.n_nodes = n_nodes
         self.runner = CudaRunner(self.ir, options=options)
+        self.build_key = self.runner.mb.so_path.stem[3:]  # lib<mech>-<hash>
         self.data = init(self.ir, n, seed)
         self.kernel = "step_nodes" if n_nodes else "step"
         if n_nodes:
             self.node_index, self.node_v = node_layout(n, n_nodes, seed)
         self.dev = None
 
+    @property
+    def kernel_name(self):
+        return f"{self.runner.mb.symbol}_k_{self.kernel}"
+
     def setup_device(self):
-        import ctypes as C
-
-        from paper_1905_02241_b200 import runtime as rt
-
         r = self.runner
-        self.dev = r.to_device(self.data)
         if self.n_nodes:
-            nb = r.bind_nodes(self.dev, self.node_index, self.node_v)
-            rt.check(rt.lib().nmodl_gather_v(C.c_void_p(nb.node_v), C.c_void_p(nb.node_index),
-                                             C.c_void_p(self.dev.ptr["v"]), self.n, C.c_void_p(r.stream.handle)),
-                     "gather_v")
+            self.dev = r.to_device(self.data, skip=("v",))
+            r.bind_nodes(self.dev, self.node_index, self.node_v)
+            r.gather_voltage(self.dev)
+        else:
+            self.dev = r.to_device(self.data)
         r.run_kernel(self.dev, "initialize", 1)
         # the store is resident now: drop the host copy (8 ranks x GBs of numpy otherwise)
         self.data = None
@@ -304,14 +376,31 @@ class Population:
         return launch_bytes(self.runner.abi, self.n, self.kernel, touched)
 
 
-# device-side head start (nmodl_spin) before host-issued timed launches: the
-# per-launch ctypes overhead -- and a GIL hand-off to the NVML clock sampler
-# thread (5 ms switch interval) -- must not show up as GPU idle time between
-# the events
-HEAD_START_NS = 12_000_000
+class L2Flush:
+    """Between timed steps of an L2-sized workload: write a 2 x L2 buffer
+    (evicts every line the previous step left in L2), then read a second
+    2 x L2 buffer so the flush's own dirty lines are written back before
+    the next step starts instead of during it (tools/micro/flush_modes.cu)."""
+
+    def __init__(self, l2_bytes):
+        from paper_1905_02241_b200 import runtime as rt
+
+        self.rt = rt
+        self.w = rt.DeviceBuffer(2 * l2_bytes)
+        self.r = rt.DeviceBuffer(2 * l2_bytes)
+        rt.memset(self.r.ptr, 0, self.r.nbytes, rt.Stream())
+        rt.lib().nmodl_device_sync()
+
+    def __call__(self, stream):
+        L = self.rt.lib()
+        self.rt.check(L.nmodl_l2_flush(C_void(self.w.ptr), self.w.nbytes // 8, C_void(stream.handle)), "l2_flush")
+        self.rt.check(L.nmodl_l2_clean(C_void(self.r.ptr), self.r.nbytes // 8, C_void(stream.handle)), "l2_clean")
 
 
-def run_workload(name, args, dist, stream_timing=True):
+SUSTAINED_S = 0.6
+
+
+def run_workload(name, args, dist, sustained=True):
     from paper_1905_02241_b200 import runtime as rt
 
     w = WORKLOADS[name]
@@ -323,15 +412,11 @@ def run_workload(name, args, dist, stream_timing=True):
     for dst, dslot, src, sslot in w.get("couplings", ()):
         by_stem[dst].runner.share_slot(by_stem[dst].dev, dslot, by_stem[src].dev, sslot)
     info = rt.device_info(dist.device)
-    streams = [p.runner.stream for p in pops]
     working = sum(p.launch_bytes() for p in pops)
-    flush = working < 3 * info["l2_bytes"]
-    flush_buf = rt.DeviceBuffer(2 * info["l2_bytes"]) if flush else None
-    s0 = streams[0]
-    # all populations on one stream so the step sequence is ordered
-    for p in pops:
+    flush = L2Flush(info["l2_bytes"]) if working < 3 * info["l2_bytes"] else None
+    s0 = pops[0].runner.stream
+    for p in pops:  # one stream: launch order == step order (bbp20m's coupling)
         p.runner.stream = s0
-    ev_a, ev_b = rt.Event(), rt.Event()
     K, W = args.steps, args.warmup
     for _ in range(W):
         for p in pops:
@@ -339,113 +424,124 @@ def run_workload(name, args, dist, stream_timing=True):
     s0.sync()
     for p in pops:
         p.runner.check(p.dev)
-    # per-kernel timing (launch duration of the dominant kernel) + step time
-    per_pop_ms = [0.0] * len(pops)
-    evs = [(rt.Event(), rt.Event()) for _ in pops]
+    # the timed graph: K steps, an external event record before the step and
+    # after every population's launch (kernel durations inside this replay)
+    P = len(pops)
+    evs = [[rt.Event() for _ in range(P + 1)] for _ in range(K)]
+
+    def body():
+        for k in range(K):
+            if flush is not None:
+                flush(s0)
+            evs[k][0].record_external(s0)
+            for j, p in enumerate(pops):
+                p.launch(1)
+                evs[k][j + 1].record_external(s0)
+
+    graph = rt.capture(s0, body)
+    ev_a, ev_b = rt.Event(), rt.Event()
     dist.barrier()
     s0.sync()
-    total_ms = 0.0
-    visible = os.environ.get("CUDA_VISIBLE_DEVICES")
-    phys = int(visible.split(",")[dist.device]) if visible and visible.split(",")[0].isdigit() else dist.device
+    phys = _physical_gpu(dist.device)
     with ClockSampler(phys) as clk:
-        if flush:
-            for _ in range(K):
-                # head start so the host enqueues the whole step before the GPU reaches it
-                rt.check(rt.lib().nmodl_spin(HEAD_START_NS, C_void(s0.handle)), "spin")
-                rt.check(rt.lib().nmodl_l2_flush(C_void(flush_buf.ptr), flush_buf.nbytes // 8, C_void(s0.handle)), "flush")
-                ev_a.record(s0)
-                if len(pops) == 1:  # no inner events: the step IS the launch
-                    pops[0].launch(1)
-                else:
-                    for j, p in enumerate(pops):
-                        evs[j][0].record(s0)
-                        p.launch(1)
-                        evs[j][1].record(s0)
-                ev_b.record(s0)
-                ev_b.sync()
-                step_ms = ev_a.elapsed_ms(ev_b)
-                total_ms += step_ms
-                for j in range(len(pops)):
-                    per_pop_ms[j] += step_ms if len(pops) == 1 else evs[j][0].elapsed_ms(evs[j][1])
-        else:
-            graph = rt.capture(s0, lambda: [p.launch(1) for _ in range(K) for p in pops])
-            ev_a.record(s0)
-            graph.launch(s0)
-            ev_b.record(s0)
-            ev_b.sync()
-            total_ms = ev_a.elapsed_ms(ev_b)
-            # separate pass: per-population launch durations (same stream, events between kernels)
-            for _ in range(min(K, 10)):
-                rt.check(rt.lib().nmodl_spin(HEAD_START_NS, C_void(s0.handle)), "spin")
-                for j, p in enumerate(pops):
-                    evs[j][0].record(s0)
-                    p.launch(1)
-                    evs[j][1].record(s0)
-                s0.sync()
-                for j in range(len(pops)):
-                    per_pop_ms[j] += evs[j][0].elapsed_ms(evs[j][1]) * (K / min(K, 10))
-    s0.sync()
+        ev_a.record(s0)
+        graph.launch(s0)
+        ev_b.record(s0)
+        ev_b.sync()
+    graph_ms = ev_a.elapsed_ms(ev_b)
+    per_pop_ms = [sum(evs[k][j].elapsed_ms(evs[k][j + 1]) for k in range(K)) for j in range(P)]
+    steps_ms = sum(evs[k][0].elapsed_ms(evs[k][P]) for k in range(K))
+    # with a flush the timed region is the steps only (flush kernels excluded)
+    total_ms = steps_ms if flush is not None else graph_ms
+    del graph
     for p in pops:
         p.runner.check(p.dev)
     clocks = clk.summary()
+    sus = None
+    if sustained and flush is None:
+        S = int(min(20000, max(K, SUSTAINED_S / max(total_ms / K / 1e3, 1e-9))))
+        g2 = rt.capture(s0, lambda: [p.launch(1) for _ in range(S) for p in pops])
+        dist.barrier()
+        s0.sync()
+        with ClockSampler(phys) as clk2:
+            ev_a.record(s0)
+            g2.launch(s0)
+            ev_b.record(s0)
+            ev_b.sync()
+        sms = ev_a.elapsed_ms(ev_b)
+        del g2
+        for p in pops:
+            p.runner.check(p.dev)
+        smax = dist.allreduce([sms], "max")[0]
+        n_all_s = dist.allreduce([float(sum(p.n for p in pops))], "sum")[0]
+        sus = {"value": n_all_s * S / (smax / 1e3), "ms_per_step": smax / S, "steps": S, "seconds": smax / 1e3,
+               "clocks": clk2.summary(),
+               "note": f"one graph of {S} steps (>= {SUSTAINED_S} s) right after the timed burst"}
     dist.barrier()
     max_ms = dist.allreduce([total_ms], "max")[0]
     n_rank = sum(p.n for p in pops)
     n_all = dist.allreduce([float(n_rank)], "sum")[0]
     value = n_all * K / (max_ms / 1e3)
-    # roofline of the dominant kernel (largest share of the step)
     j = int(np.argmax(per_pop_ms))
     dom = pops[j]
-    dom_ms = per_pop_ms[j] / K
-    peak, peak_src = _peaks()
-    achieved = dom.launch_bytes() / (dom_ms / 1e3) / 1e9
-    from paper_1905_02241_b200.traffic import describe
-
-    from paper_1905_02241_b200.parallel import device_checksums, gather_checksums
+    sm_mhz = clocks.get("sm_mhz")
+    roof = _roofline(dom.kernel_name, dom.launch_bytes(), _fp64_ops(dom.ir) * dom.n, per_pop_ms[j] / K,
+                     [dom.build_key], sm_mhz)
+    roof["share_of_step"] = per_pop_ms[j] / max(sum(per_pop_ms), 1e-30)
+    roof["model"] = _describe(dom)
+    from paper_1905_02241_b200.parallel import device_checksums
 
     local = np.concatenate([device_checksums(p.runner, p.dev) for p in pops])
-    table = gather_checksums(local, device=dist.tensor_device)
-    res = {
+    table = dist.allgather(local)
+    per_mech = {}
+    for i, p in enumerate(pops):
+        ms = per_pop_ms[i] / K
+        r = _roofline(p.kernel_name, p.launch_bytes(), _fp64_ops(p.ir) * p.n, ms, [p.build_key], sm_mhz)
+        per_mech[p.stem] = {"instances": p.n, "ms_per_launch": ms, "GBps": r["achieved"], "hbm_frac": r["frac"],
+                            "fp64_frac": r["fp64"]["frac"], "bound": r["bound"], "traffic": r["traffic"],
+                            "bytes_per_instance_step": p.launch_bytes() / p.n, "build": p.build_key}
+    return {
         "value": value,
         "checksum_of_checksums": float(np.sum(table[..., 1])),
         "ms_per_step": max_ms / K,
         "n_rank": n_rank,
         "clocks": clocks,
-        "gpu_launches": K * len(pops),
-        "l2": "L2 flushed between timed steps" if flush else "inputs larger than L2 (no flush)",
-        "roofline": {
-            "bound": "hbm",
-            "kernel": f"{dom.runner.mb.symbol}_k_{dom.kernel}",
-            "achieved": achieved,
-            "peak": peak,
-            "unit": "GB/s",
-            "frac": achieved / peak,
-            "traffic": _ncu_traffic(name),
-            "peak_source": peak_src,
-            "bytes_per_launch": dom.launch_bytes(),
-            "model": describe(dom.runner.abi, dom.kernel),
-            "share_of_step": per_pop_ms[j] / max(sum(per_pop_ms), 1e-30),
-            "launch_ms": dom_ms,
-        },
-        "per_mechanism": {
-            p.stem: {"instances": p.n, "ms_per_launch": per_pop_ms[i] / K,
-                     "GBps": p.launch_bytes() / (per_pop_ms[i] / K / 1e3) / 1e9,
-                     "bytes_per_instance_step": p.launch_bytes() / p.n}
-            for i, p in enumerate(pops)
-        },
-        "pops": pops,
+        "sustained": sus,
+        "gpu_launches": K * P,
+        "l2": ("L2 flushed between timed steps (write 2xL2, then read 2xL2 clean; flush kernels outside the "
+               "event-timed steps)") if flush is not None else "inputs larger than L2 (no flush)",
+        "roofline": roof,
+        "per_mechanism": per_mech,
     }
-    return res
 
 
-def run_column(args, dist):
+def _describe(pop):
+    from paper_1905_02241_b200.traffic import describe
+
+    return describe(pop.runner.abi, pop.kernel)
+
+
+def _physical_gpu(device):
+    visible = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if visible and visible.split(",")[0].isdigit():
+        return int(visible.split(",")[device])
+    return device
+
+
+def _column_spec():
+    from paper_1905_02241_b200.column import ColumnSpec
+
+    return ColumnSpec(n_cells=WORKLOADS["column"]["cells"])
+
+
+def run_column(args, dist, sustained=True):
     """configs[4]: 100k-cell synthetic column, cells partitioned over ranks by
     per-cell bytes/step (parallel.partition_cells); strong scaling."""
     from paper_1905_02241_b200 import runtime as rt
-    from paper_1905_02241_b200.column import ColumnShard, ColumnSpec
-    from paper_1905_02241_b200.parallel import gather_checksums, partition_cells
+    from paper_1905_02241_b200.column import LAUNCH_ORDER, ColumnShard
+    from paper_1905_02241_b200.parallel import partition_cells
 
-    spec = ColumnSpec(n_cells=WORKLOADS["column"]["cells"])
+    spec = _column_spec()
     bounds = partition_cells(np.full(spec.n_cells, spec.cell_cost()), dist.world)
     shard = ColumnShard(spec, int(bounds[dist.rank]), int(bounds[dist.rank + 1]), options_for,
                         concurrent_soma=os.environ.get("NMODL_COLUMN_SEQUENTIAL") is None)
@@ -457,20 +553,37 @@ def run_column(args, dist):
     ev_a, ev_b = rt.Event(), rt.Event()
     graph = rt.capture(s0, lambda: shard.launch(K))
     dist.barrier()
-    visible = os.environ.get("CUDA_VISIBLE_DEVICES")
-    phys = int(visible.split(",")[dist.device]) if visible and visible.split(",")[0].isdigit() else dist.device
+    s0.sync()
+    phys = _physical_gpu(dist.device)
     with ClockSampler(phys) as clk:
         ev_a.record(s0)
         graph.launch(s0)
         ev_b.record(s0)
         ev_b.sync()
     ms = ev_a.elapsed_ms(ev_b)
+    del graph
     shard.check()
-    # per-population launch durations (separate pass, events between kernels)
-    from paper_1905_02241_b200.column import LAUNCH_ORDER
-
-    # (each population's launches captured in its own graph, so host launch
-    # latency does not pollute the small populations' times)
+    clocks = clk.summary()
+    sus = None
+    if sustained:
+        S = int(min(20000, max(K, SUSTAINED_S / max(ms / K / 1e3, 1e-9))))
+        g2 = rt.capture(s0, lambda: shard.launch(S))
+        dist.barrier()
+        s0.sync()
+        with ClockSampler(phys) as clk2:
+            ev_a.record(s0)
+            g2.launch(s0)
+            ev_b.record(s0)
+            ev_b.sync()
+        sms = ev_a.elapsed_ms(ev_b)
+        del g2
+        shard.check()
+        smax = dist.allreduce([sms], "max")[0]
+        n_all_s = dist.allreduce([float(shard.n_instances)], "sum")[0]
+        sus = {"value": n_all_s * S / (smax / 1e3), "ms_per_step": smax / S, "steps": S, "seconds": smax / 1e3,
+               "clocks": clk2.summary()}
+    # per-population launch durations: each population's launches alone in
+    # their own graph (the soma populations overlap inside the real step)
     per_pop = {}
     reps = 10
     for m in LAUNCH_ORDER:
@@ -485,23 +598,32 @@ def run_column(args, dist):
     dist.barrier()
     max_ms = dist.allreduce([ms], "max")[0]
     n_all = dist.allreduce([float(shard.n_instances)], "sum")[0]
-    table = gather_checksums(shard.checksums(), device=dist.tensor_device)
-    peak, peak_src = _peaks()
-    achieved = shard.launch_bytes() / (ms / K / 1e3) / 1e9
+    table = dist.allgather(shard.checksums())
+    from paper_1905_02241_b200.traffic import launch_bytes
+
+    fp64 = sum(_fp64_ops(shard.runners[m].ir) * shard.devs[m].n for m in LAUNCH_ORDER)
+    keys = [shard.runners[m].mb.so_path.stem[3:] for m in LAUNCH_ORDER]
+    roof = _roofline("7 x <mech>_k_step_nodes + soma combine (whole step)", shard.launch_bytes(), fp64, ms / K, keys,
+                     clocks.get("sm_mhz"))
+    roof["share_of_step"] = 1.0
+    per_mech = {}
+    for m in LAUNCH_ORDER:
+        d, r = shard.devs[m], shard.runners[m]
+        b = launch_bytes(r.abi, d.n, "step_nodes", d.nodes.n_segs)
+        per_mech[m] = {"instances": d.n, "ms_per_launch_alone": per_pop[m], "GBps_alone": b / (per_pop[m] / 1e3) / 1e9,
+                       "segments": d.nodes.n_segs, "build": r.mb.so_path.stem[3:]}
     return {
         "value": n_all * K / (max_ms / 1e3),
         "ms_per_step": max_ms / K,
         "n_rank": shard.n_instances,
-        "clocks": clk.summary(),
-        "gpu_launches": K * 7,
+        "clocks": clocks,
+        "sustained": sus,
+        "gpu_launches": K * shard.kernels_per_step(),
         "l2": "inputs larger than L2 (no flush)",
-        "roofline": {"bound": "hbm", "kernel": "7 x <mech>_k_step_nodes (whole step)", "achieved": achieved,
-                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                     "bytes_per_launch": shard.launch_bytes()},
+        "roofline": roof,
         "checksum_of_checksums": float(np.sum(table[..., 1])),
         "cells_per_rank": [int(b) for b in np.diff(bounds)],
-        "per_mechanism": {m: {"instances": shard.devs[m].n, "ms_per_launch": per_pop[m],
-                              "segments": shard.devs[m].nodes.n_segs} for m in shard.devs},
+        "per_mechanism": per_mech,
     }
 
 
@@ -557,17 +679,27 @@ def e2e_measure(name, dist, calls=2, timesteps=1000):
     phases["unaccounted"] = dt - sum(phases.values())
     dt = dist.allreduce([dt], "max")[0]
     n_all = dist.allreduce([float(sum(j[5] for j in jobs))], "sum")[0]
-    return {
-        "value": n_all * timesteps * calls / dt,
-        "unit": UNIT,
-        "h2d_bytes_per_step": int(sum(_h2d(j) for j in jobs)),
-        "d2h_bytes_per_step": int(sum(_d2h(j) for j in jobs)),
-        "step": f"one public-API call: pinned H2D of the store, nrn_init, {timesteps} timesteps, D2H of the store"
-                + (", node_index upload + device sort, node rhs/d download" if w["nodes"] else ""),
-        "timesteps_per_call": timesteps,
-        "calls": calls,
-        "phase_seconds_per_call": {k: v / calls for k, v in phases.items()},
-    }
+    h2d = int(sum(_h2d(j) for j in jobs))
+    d2h = int(sum(_d2h(j) for j in jobs))
+    return _e2e_line(n_all * timesteps * calls / dt, h2d, d2h, timesteps, calls,
+                     f"one public-API call (runner.simulate{'_nodes' if w['nodes'] else ''}): pinned H2D of the store"
+                     + (", node_index + node_v upload, device sort" if w["nodes"] else "")
+                     + f", nrn_init, {timesteps} timesteps, D2H of the written arrays"
+                     + (" and node rhs/d" if w["nodes"] else ""),
+                     {k: v / calls for k, v in phases.items()})
+
+
+def _e2e_line(value, h2d_call, d2h_call, timesteps, calls, step, phases=None):
+    """The e2e object: the copy fields of the contract are per timestep (one
+    public call = `timesteps` steps, one upload and one download); the
+    per-call bytes are stated beside them."""
+    out = {"value": value, "unit": UNIT,
+           "h2d_bytes_per_step": h2d_call / timesteps, "d2h_bytes_per_step": d2h_call / timesteps,
+           "h2d_bytes_per_call": h2d_call, "d2h_bytes_per_call": d2h_call,
+           "timesteps_per_call": timesteps, "calls": calls, "call": step}
+    if phases is not None:
+        out["phase_seconds_per_call"] = phases
+    return out
 
 
 def _h2d(job):
@@ -594,53 +726,51 @@ def _d2h(job):
     return b
 
 
+def e2e_column(dist, calls=1, timesteps=1000):
+    """configs[4] through the public column call (column.simulate_column):
+    pinned H2D of this rank's seven stores, the node voltages and node_index
+    arrays, the device-side node layout, nrn_init, `timesteps` steps of all
+    populations, D2H of every written array and the node arrays."""
+    from paper_1905_02241_b200 import runtime as rt
+    from paper_1905_02241_b200.column import LAUNCH_ORDER, host_stores, shard_layout, simulate_column
+    from paper_1905_02241_b200.parallel import partition_cells
+
+    spec = _column_spec()
+    bounds = partition_cells(np.full(spec.n_cells, spec.cell_cost()), dist.world)
+    lo, hi = int(bounds[dist.rank]), int(bounds[dist.rank + 1])
+    host = host_stores(spec, lo, hi)
+    pins = [rt.PinnedRegistration(a) for h in host.values() for a in list(h.arrays.values()) + list(h.acc.values())]
+    lay = shard_layout(spec, lo, hi)
+    conc = os.environ.get("NMODL_COLUMN_SEQUENTIAL") is None
+    # warm-up call: loads the kernels (reused below), primes the caches
+    _, _, shard = simulate_column(spec, 10, lo, hi, host=host, options_for=options_for, concurrent_soma=conc)
+    runners = shard.runners
+    writes = {m: runners[m]._writes["initialize"] | runners[m]._writes["step_nodes"] | {"v"} for m in LAUNCH_ORDER}
+    del shard
+    host = host_stores(spec, lo, hi)  # fresh inputs (the warm-up advanced them)
+    pins = [rt.PinnedRegistration(a) for h in host.values() for a in list(h.arrays.values()) + list(h.acc.values())]
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(calls):
+        _, nodes, shard = simulate_column(spec, timesteps, lo, hi, host=host, options_for=options_for,
+                                          runners=runners, concurrent_soma=conc)
+    dt = time.perf_counter() - t0
+    dt = dist.allreduce([dt], "max")[0]
+    n_rank = sum(h.n for h in host.values())
+    n_all = dist.allreduce([float(n_rank)], "sum")[0]
+    h2d = sum(a.nbytes for h in host.values() for a in h.arrays.values())
+    h2d += sum(idx.nbytes for _, _, idx in lay["mechs"].values()) + lay["node_v"].nbytes
+    d2h = sum(8 * host[m].n for m in LAUNCH_ORDER for k in list(host[m].arrays) + ["i_acc", "g_acc"] if k in writes[m])
+    d2h += 3 * 8 * lay["n_nodes"]
+    del pins
+    return _e2e_line(n_all * timesteps * calls / dt, h2d, d2h, timesteps, calls,
+                     "one public column call (column.simulate_column): pinned H2D of the 7 stores, node_v and "
+                     f"node_index, device node layout, nrn_init, {timesteps} timesteps, D2H of the written arrays "
+                     "and node v/rhs/d")
+
+
 # ---------------------------------------------------------------------------
 # CPU reference (the reference's emitted C, all host threads)
-
-
-def cpu_reference(name, target_s=10.0, max_n=2_000_000, steps_cap=200):
-    from oracle import ref_c
-    from paper_1905_02241_b200.instance import init
-    from paper_1905_02241_b200.ir import MechIR
-
-    w = WORKLOADS[name]
-    threads = os.cpu_count() or 1
-    per_mech = []
-    total_inst_steps = 0.0
-    total_s = 0.0
-    for stem, n in w["mechs"]:
-        if not ref_c.available(stem):
-            return None
-        so = ref_c.native_build(stem)
-        r = ref_c.RefC(stem, so)
-        ir = MechIR.load(ROOT / "fixtures" / "ir" / f"{stem}.json")
-        ns = min(n, max_n)
-        data = init(ir, ns, 42)
-        r.initialize(data)
-        t0 = time.perf_counter()
-        r.steps(data, 2, threads)
-        dt1 = (time.perf_counter() - t0) / 2
-        steps = int(max(2, min(steps_cap, (target_s / len(w["mechs"])) / max(dt1, 1e-6))))
-        t0 = time.perf_counter()
-        r.steps(data, steps, threads)
-        dt = time.perf_counter() - t0
-        per_mech.append(f"{stem}: {ns} instances x {steps} steps in {dt:.2f}s")
-        # time-weighted combination: the population's full step is the sum of its mechanisms
-        total_s += dt * (n / ns) / steps
-        total_inst_steps += n
-    value = total_inst_steps / total_s
-    return {
-        "value": value,
-        "unit": UNIT,
-        "cores": threads,
-        "kind": "reference",
-        "numpy_oracle": numpy_oracle_rate(name),
-        "sample": "reference-emitted scalar C (modlc.codegen.emit_scalar, count field renamed), gcc -O3 "
-                  "-march=native, contiguous shards per thread, accumulators zeroed per step; "
-                  + "; ".join(per_mech)
-                  + ("; no node_index scatter (the reference has none)" if w["nodes"] else ""),
-        "cpu": _cpu_model(),
-    }
 
 
 def numpy_oracle_rate(name, n=65536, budget_s=4.0):
@@ -651,18 +781,16 @@ def numpy_oracle_rate(name, n=65536, budget_s=4.0):
     from oracle import interp_np as O
     from paper_1905_02241_b200.ir import MechIR
 
-    w = WORKLOADS[name]
-    if not w["mechs"]:
-        return None
+    mechs = _reference_mechs(name)
     total_s, total_n, parts = 0.0, 0, []
-    for stem, n_full in w["mechs"]:
+    for stem, n_full in mechs:
         ir = MechIR.load(ROOT / "fixtures" / "ir" / f"{stem}.json")
         data = O.init(ir, n, 42)
         runner = O.OracleRunner(ir)
         runner.run_kernel(data, "initialize", 1)
         steps, dt = 0, 0.0
         t0 = time.perf_counter()
-        while dt < budget_s / len(w["mechs"]) or steps < 2:
+        while dt < budget_s / len(mechs) or steps < 2:
             runner.run_kernel(data, "state_update", 1)
             runner.run_kernel(data, "current_update", 1)
             steps += 1
@@ -674,24 +802,28 @@ def numpy_oracle_rate(name, n=65536, budget_s=4.0):
             "sample": "oracle/interp_np.py (numpy restatement of modlc.interp.Runner), single thread; " + "; ".join(parts)}
 
 
+def _reference_mechs(name):
+    if name == "column":
+        from paper_1905_02241_b200.column import LAUNCH_ORDER
+
+        spec = _column_spec()
+        return [(m, spec.n_cells * spec.instances_per_cell(m)) for m in LAUNCH_ORDER]
+    return WORKLOADS[name]["mechs"]
+
+
 def reference_arm(name, K, W, budget_s=60.0):
-    """`--impl reference`: W untimed + K timed steps of the reference CPU path
-    (emitted scalar C, all host threads).  Each step advances one timestep of
-    a bounded instance sample per mechanism, sized so the whole run takes
-    about `budget_s`; the full-population step time is extrapolated linearly
-    in the instance count (the C loop is per-instance independent)."""
+    """The reference's CPU path: W untimed + K timed steps of its emitted
+    scalar C (all host threads).  Each step advances one timestep of a
+    bounded instance sample per mechanism, sized so the whole run takes about
+    `budget_s`; the full-population step time is the sample's time scaled by
+    n / sample (the C loop is per-instance independent).  Used by
+    `--impl reference` and, with a smaller K, as the ours-arm cpu_baseline."""
     from oracle import ref_c
     from paper_1905_02241_b200.instance import init
     from paper_1905_02241_b200.ir import MechIR
 
-    w = WORKLOADS[name]
     threads = os.cpu_count() or 1
-    mechs = w["mechs"]
-    if name == "column":
-        from paper_1905_02241_b200.column import LAUNCH_ORDER, ColumnSpec
-
-        spec = ColumnSpec(n_cells=w["cells"])
-        mechs = [(m, spec.n_cells * spec.instances_per_cell(m)) for m in LAUNCH_ORDER]
+    mechs = _reference_mechs(name)
     jobs = []
     for stem, n in mechs:
         if not ref_c.available(stem):
@@ -726,8 +858,10 @@ def reference_arm(name, K, W, budget_s=60.0):
         "cores": threads,
         "kind": "reference",
         "sample": "reference-emitted scalar C (modlc.codegen.emit_scalar, count field renamed), gcc -O3 -march=native, "
-                  f"{threads} threads, per step: " + ", ".join(f"{stem} {ns} of {n} instances" for stem, n, ns, _, _ in jobs)
-                  + ("; no node_index scatter (the reference has none)" if w["nodes"] else ""),
+                  f"{threads} threads, {K} timed steps after {W}, each step: "
+                  + ", ".join(f"{stem} {ns} of {n} instances" for stem, n, ns, _, _ in jobs)
+                  + (" (full-population time = sample time x n/sample)")
+                  + ("; no node_index scatter (the reference has none)" if WORKLOADS[name]["nodes"] else ""),
         "cpu": _cpu_model(),
     }
 
@@ -754,89 +888,89 @@ def main():
     ap.add_argument("--workload", choices=list(WORKLOADS), default=DEFAULT_WORKLOAD)
     ap.add_argument("--no-also", action="store_true", help="skip the secondary workloads")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-sustained", action="store_true")
     args = ap.parse_args()
-    dist = Dist()
     w = WORKLOADS[args.workload]
+    column = args.workload == "column"
     config = {
         "workload": args.workload,
         "baseline_config": w["config"],
-        "mechanisms": {stem: n for stem, n in w["mechs"]},
-        "instances_per_gpu": sum(n for _, n in w["mechs"]),
+        "mechanisms": {stem: n for stem, n in _reference_mechs(args.workload)},
+        "instances_per_gpu": None if column else sum(n for _, n in w["mechs"]),
         "n_nodes_per_gpu": w["nodes"],
         "dt_ms": 0.025,
-        "parallelism": f"{args.gpus} x instance shard by cell (weak scaling, no per-step collective)",
+        "parallelism": (f"{args.gpus} x cell shard (strong scaling, no per-step collective)" if column else
+                        f"{args.gpus} x instance shard by cell (weak scaling, no per-step collective)"),
     }
+    if column:
+        config["cells"] = w["cells"]
+    line = {"metric": METRIC, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "strong" if column else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (modlc.interp.init-format seeded instance store; random node_index)",
+            "config": config}
     if args.impl == "reference":
-        if dist.rank == 0:
-            K, W = args.steps, args.warmup
-            ref = reference_arm(args.workload, K, W)
-            line = {"impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": args.gpus, "steps": K,
-                    "warmup": W, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                    "data": "synthetic (modlc.interp.init-format seeded instance store)", "config": config}
+        rank = int(os.environ.get("RANK", "0"))
+        if rank == 0:
+            ref = reference_arm(args.workload, args.steps, args.warmup)
+            line["impl"] = "reference"
             if ref is None:
-                line.update({"unavailable": "oracle/_ref not built (needs the reference front-end)"})
+                line["unavailable"] = "oracle/_ref not built (needs the reference front-end)"
             else:
                 line.update({"value": ref["value"], "ms_per_step": ref["ms_per_step"],
                              "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu")},
-                             "e2e": {"value": ref["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+                             "e2e": {"value": ref["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                                     "d2h_bytes_per_step": 0}})
             print(json.dumps(line), flush=True)
-        dist.close()
         return
+    dist = Dist()
     from paper_1905_02241_b200 import runtime as rt
 
     rt.require_device(dist.device)
-    if args.workload == "column":
-        res = run_column(args, dist)
-        e2e = None
-        config["cells"] = WORKLOADS["column"]["cells"]
-        config["instances_per_gpu"] = None
-        config["parallelism"] = f"{args.gpus} x cell shard (strong scaling, no per-step collective; NCCL checksum gather)"
+    if column:
+        res = run_column(args, dist, sustained=not args.no_sustained)
+        e2e = None if args.no_e2e else e2e_column(dist)
     else:
-        res = run_workload(args.workload, args, dist)
+        res = run_workload(args.workload, args, dist, sustained=not args.no_sustained)
         e2e = None if args.no_e2e else e2e_measure(args.workload, dist)
     also = {}
-    if not args.no_also and args.workload != "column":
-        for other in ("hh1m", "bbp20m", "kinetic1m"):
+    if not args.no_also and not column:
+        for other in ("hh1m", "hh10m", "bbp20m", "kinetic1m"):
             if other == args.workload:
                 continue
             # warm-up past the initial transient: Newton iteration counts
             # (cdp5ish) fall over the first ~100 steps after nrn_init
             a = argparse.Namespace(steps=min(args.steps, 50), warmup=max(args.warmup, 100))
-            r = run_workload(other, a, dist)
+            r = run_workload(other, a, dist, sustained=False)
             also[other] = {"value": r["value"], "ms_per_step": r["ms_per_step"], "l2": r["l2"],
-                           "roofline": {k: r["roofline"][k] for k in ("kernel", "achieved", "peak", "frac", "bytes_per_launch", "launch_ms")},
-                           "per_mechanism": r["per_mechanism"]}
+                           "roofline": r["roofline"], "per_mechanism": r["per_mechanism"]}
             del r
     cpu = None
-    if dist.rank == 0 and args.gpus == 1 and args.workload != "column":
-        cpu = cpu_reference(args.workload)
+    if dist.rank == 0 and args.gpus == 1 and not args.no_cpu:
+        cpu = reference_arm(args.workload, K=3, W=1, budget_s=20.0)
+        if cpu is not None and not column:
+            cpu["numpy_oracle"] = numpy_oracle_rate(args.workload)
     if dist.rank == 0:
-        config["l2_policy"] = res["l2"]
-        config["arithmetic"] = RELAXED_NOTE
-        line = {
-            "metric": METRIC,
+        line.update({
             "value": res["value"],
-            "unit": UNIT,
-            "n_gpus": args.gpus,
-            "steps": args.steps,
-            "warmup": args.warmup,
             "ms_per_step": res["ms_per_step"],
-            "higher_is_better": True,
-            "scaling": "strong" if args.workload == "column" else "weak",
-            "vs_baseline": None,
-            "dtype": "f64",
-            "data": "synthetic (modlc.interp.init-format seeded instance store; random node_index)",
-            "config": config,
             "roofline": res["roofline"],
-            "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu", "numpy_oracle")},
+            "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                                          "cpu", "numpy_oracle") if k in cpu},
             "e2e": e2e,
             "gpu_launches": res["gpu_launches"],
             "clocks": res["clocks"],
+            "sustained": res["sustained"],
+            "l2": res["l2"],
+            "arithmetic": RELAXED_NOTE,
             "per_mechanism": res["per_mechanism"],
             "validation": {"checksum_of_checksums": res.get("checksum_of_checksums"),
-                           "how": "per-array sum|x| on each GPU (fixed-tree device reduction), all-gathered with NCCL"},
+                           "how": f"per-array sum|x| on each GPU (fixed-tree device reduction), all-gathered "
+                                  f"({dist.backend} process group)"},
             "also": also,
-        }
+        })
+        if column:
+            line["cells_per_rank"] = res["cells_per_rank"]
         print(json.dumps(line), flush=True)
     dist.close()
 

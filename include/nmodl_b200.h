@@ -110,6 +110,8 @@ int nmodl_first_nonfinite(const double *p, long long n, unsigned long long *out_
 int nmodl_checksum(const double *p, long long n, double *scratch_dev, double *out_dev, nmodl_stream_t s);
 /* write a buffer larger than L2 (timing hygiene) */
 int nmodl_l2_flush(double *buf, long long n_doubles, nmodl_stream_t s);
+/* read a (zeroed) buffer larger than L2: cleans L2 after nmodl_l2_flush */
+int nmodl_l2_clean(const double *buf, long long n_doubles, nmodl_stream_t s);
 /* keep the stream busy for `ns` nanoseconds (one spinning thread) so host-issued
  * timed launches queue up behind it instead of leaving gaps in the timing */
 int nmodl_spin(long long ns, nmodl_stream_t s);

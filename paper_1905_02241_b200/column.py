@@ -227,6 +227,11 @@ class ColumnShard:
                 if stem not in SOMA_MECHS:
                     self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
 
+    def kernels_per_step(self) -> int:
+        """Our kernels per timestep: one fused step per population, plus the
+        soma combine in concurrent mode."""
+        return len(LAUNCH_ORDER) + (1 if self.concurrent else 0)
+
     def check(self) -> None:
         for stem in LAUNCH_ORDER:
             self.runners[stem].check(self.devs[stem])

@@ -83,6 +83,7 @@ _SIGS = {
     "nmodl_first_nonfinite": (C.c_int, [C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p]),
     "nmodl_checksum": (C.c_int, [C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p]),
     "nmodl_l2_flush": (C.c_int, [C.c_void_p, C.c_longlong, C.c_void_p]),
+    "nmodl_l2_clean": (C.c_int, [C.c_void_p, C.c_longlong, C.c_void_p]),
     "nmodl_spin": (C.c_int, [C.c_longlong, C.c_void_p]),
     "nmodl_scatter_layout": (
         C.c_int,

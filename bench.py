@@ -92,7 +92,7 @@ def options_for(stem: str):
     from paper_1905_02241_b200.codegen_cuda import CudaOptions
 
     tuned = {
-        "ProbAMPANMDA_EMS": CudaOptions(ilp=1, fast_path=False, tile=2304),  # 2048: 0.2823, 2304: 0.2807 ms (3 reps)
+        "ProbAMPANMDA_EMS": CudaOptions(ilp=1, fast_path=False, tile=2304, min_blocks=4),  # 2048: 0.2823, 2304: 0.2807 ms (3 reps); min_blocks=4 keeps it at <= 64 registers (4 CTAs/SM)
         "hh_subset": CudaOptions(ilp=1, pipe=True, recip=True, div_approx=True, exp_share=True,
                                  fast_redo=True),  # 0.0412 -> 0.0329 ms
         "NaTs2_t": CudaOptions(ilp=2, min_blocks=2, pipe=True, recip=True, div_approx=True, exp_share=True,
@@ -270,10 +270,11 @@ def _traffic_record():
 
 
 def _traffic(build_keys):
-    """ncu DRAM bytes (read + write) per launch of these exact builds (the
-    content-addressed library stem: generated text + flags + headers), from
-    `ncu --set full` captures of the same bench configuration
-    (tools/profile_bench.py); None unless every build was captured."""
+    """ncu DRAM bytes (read + write) per launch of these exact builds at these
+    population sizes ("<content-addressed library stem>@<instances>": the
+    generated text + flags + headers), from `ncu --set full` captures of the
+    same bench configuration (tools/profile_bench.py); None unless every
+    build was captured."""
     rec = _traffic_record().get("by_build", {})
     total = 0.0
     for k in build_keys:
@@ -285,17 +286,26 @@ def _traffic(build_keys):
         rec[k].get("capture", "?") for k in build_keys)
 
 
-def _fp64_ops(ir):
+def _fp64_instr(ir, n, key):
+    """FP64 pipe instructions of one launch: the ncu-measured per-instance
+    count of this exact build (DFMA+DMUL+DADD+DSETP+DMNMX, profiles/
+    ncu_traffic.json), else the static census (analysis.fp64_ops: the
+    reference census priced with the library-exact instruction sequences)."""
+    e = _traffic_record().get("by_build", {}).get(key, {})
+    if "fp64_instr_per_instance" in e:
+        return e["fp64_instr_per_instance"] * n, "ncu-measured FP64 instructions of this build"
     from paper_1905_02241_b200.analysis import fp64_ops
 
-    return fp64_ops(ir)
+    return fp64_ops(ir) * n, "static census (analysis.fp64_ops)"
 
 
-def _roofline(kernel_name, bytes_per_launch, fp64_per_launch, launch_ms, build_keys, sm_mhz):
-    """roofline object of one kernel launch: algorithmic bytes (and census FP64
-    pipe instructions) of one launch / its measured duration, against the
-    measured HBM copy peak (and the measured DFMA rate).  `bound` is the
-    static classification: the roof the kernel would reach first."""
+def _roofline(kernel_name, bytes_per_launch, fp64, launch_ms, build_keys, sm_mhz):
+    """roofline object of one kernel launch: algorithmic bytes of one launch /
+    its measured duration against the measured HBM copy peak, and FP64 pipe
+    instructions of one launch / duration against the measured DFMA rate.
+    `fp64` = (instructions, how counted).  `bound` is the static
+    classification: the roof the kernel would reach first."""
+    fp64_per_launch, fp64_src = fp64
     peak, peak_src = _peaks()
     fpeak, fpeak_src = _fp64_peak(sm_mhz)
     s = launch_ms / 1e3
@@ -317,9 +327,7 @@ def _roofline(kernel_name, bytes_per_launch, fp64_per_launch, launch_ms, build_k
         "launch_ms": launch_ms,
         "fp64": {"achieved": fp64_per_launch / s / 1e9, "peak": fpeak / 1e9, "unit": "G FP64-pipe instr/s",
                  "frac": fp64_per_launch / s / fpeak, "instr_per_launch": fp64_per_launch,
-                 "peak_source": fpeak_src,
-                 "model": "census of the fused nrn_state+nrn_cur (analysis.fp64_ops: reference census priced "
-                          "with the emitted instruction sequences)"},
+                 "peak_source": fpeak_src, "count": fp64_src},
         "max_hbm_frac_at_fp64_roof": min(1.0, t_hbm / t_fp) if t_fp > 0 else 1.0,
     }
 
@@ -485,8 +493,9 @@ def run_workload(name, args, dist, sustained=True):
     j = int(np.argmax(per_pop_ms))
     dom = pops[j]
     sm_mhz = clocks.get("sm_mhz")
-    roof = _roofline(dom.kernel_name, dom.launch_bytes(), _fp64_ops(dom.ir) * dom.n, per_pop_ms[j] / K,
-                     [dom.build_key], sm_mhz)
+    key = f"{dom.build_key}@{dom.n}"
+    roof = _roofline(dom.kernel_name, dom.launch_bytes(), _fp64_instr(dom.ir, dom.n, key), per_pop_ms[j] / K, [key],
+                     sm_mhz)
     roof["share_of_step"] = per_pop_ms[j] / max(sum(per_pop_ms), 1e-30)
     roof["model"] = _describe(dom)
     from paper_1905_02241_b200.parallel import device_checksums
@@ -496,7 +505,8 @@ def run_workload(name, args, dist, sustained=True):
     per_mech = {}
     for i, p in enumerate(pops):
         ms = per_pop_ms[i] / K
-        r = _roofline(p.kernel_name, p.launch_bytes(), _fp64_ops(p.ir) * p.n, ms, [p.build_key], sm_mhz)
+        key = f"{p.build_key}@{p.n}"
+        r = _roofline(p.kernel_name, p.launch_bytes(), _fp64_instr(p.ir, p.n, key), ms, [key], sm_mhz)
         per_mech[p.stem] = {"instances": p.n, "ms_per_launch": ms, "GBps": r["achieved"], "hbm_frac": r["frac"],
                             "fp64_frac": r["fp64"]["frac"], "bound": r["bound"], "traffic": r["traffic"],
                             "bytes_per_instance_step": p.launch_bytes() / p.n, "build": p.build_key}
@@ -531,7 +541,7 @@ def _physical_gpu(device):
 def _column_spec():
     from paper_1905_02241_b200.column import ColumnSpec
 
-    return ColumnSpec(n_cells=WORKLOADS["column"]["cells"])
+    return ColumnSpec(n_cells=int(os.environ.get("NMODL_COLUMN_CELLS", WORKLOADS["column"]["cells"])))
 
 
 def run_column(args, dist, sustained=True):
@@ -601,8 +611,9 @@ def run_column(args, dist, sustained=True):
     table = dist.allgather(shard.checksums())
     from paper_1905_02241_b200.traffic import launch_bytes
 
-    fp64 = sum(_fp64_ops(shard.runners[m].ir) * shard.devs[m].n for m in LAUNCH_ORDER)
-    keys = [shard.runners[m].mb.so_path.stem[3:] for m in LAUNCH_ORDER]
+    keys = [f"{shard.runners[m].mb.so_path.stem[3:]}@{shard.devs[m].n}" for m in LAUNCH_ORDER]
+    parts = [_fp64_instr(shard.runners[m].ir, shard.devs[m].n, k) for m, k in zip(LAUNCH_ORDER, keys)]
+    fp64 = (sum(p[0] for p in parts), "; ".join(sorted({p[1] for p in parts})))
     roof = _roofline("7 x <mech>_k_step_nodes + soma combine (whole step)", shard.launch_bytes(), fp64, ms / K, keys,
                      clocks.get("sm_mhz"))
     roof["share_of_step"] = 1.0
@@ -890,7 +901,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-sustained", action="store_true")
+    ap.add_argument("--cells", type=int, default=None,
+                    help="column only: cells of the whole column (default 100,000); e.g. 12,500 = one rank's "
+                         "share at 8 GPUs, timed on one GPU as the strong-scaling proxy")
     args = ap.parse_args()
+    if args.cells is not None:
+        os.environ["NMODL_COLUMN_CELLS"] = str(args.cells)
     w = WORKLOADS[args.workload]
     column = args.workload == "column"
     config = {
@@ -904,7 +920,7 @@ def main():
                         f"{args.gpus} x instance shard by cell (weak scaling, no per-step collective)"),
     }
     if column:
-        config["cells"] = w["cells"]
+        config["cells"] = _column_spec().n_cells
     line = {"metric": METRIC, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "scaling": "strong" if column else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (modlc.interp.init-format seeded instance store; random node_index)",

@@ -11,7 +11,9 @@ the FP64 cost uses the instruction counts of the sequences actually emitted
 
 `roofline(ir)` returns both times for one instance-step and which one binds:
     t_hbm  = bytes / HBM bandwidth        (MEASURED_PEAKS.json hbm_gbs)
-    t_fp64 = FP64 ops / FP64 rate         (148 SM x 64 FP64 lanes x clock)
+    t_fp64 = FP64 ops / FP64 rate         (the measured DFMA rate of
+             tools/micro/fp64_peak.cu, profiles/fp64_peak.json; nominal
+             148 SM x 64 FP64 lanes x clock when that file is absent)
 """
 
 from __future__ import annotations
@@ -29,6 +31,18 @@ FP64_COST = {"exp": 16, "log": 22, "sqrt": 10, "pow": 60, "div": 8, "div_const":
              "add": 1, "sub": 1, "mul": 1, "neg": 0, "cmp": 1, "fabs": 0, "ipow": 2}
 FP64_LANES_PER_SM = 64
 SM_COUNT = 148
+_ROOT = __import__("pathlib").Path(__file__).resolve().parent.parent
+
+
+def fp64_rate(clock_ghz: float = 1.965) -> float:
+    """FP64 pipe instructions per second: measured (profiles/fp64_peak.json,
+    1.705e13 DFMA/s on B200 = 58.7 per SM per clock), else nominal."""
+    import json
+
+    p = _ROOT / "profiles" / "fp64_peak.json"
+    if p.is_file():
+        return float(json.loads(p.read_text())["dfma_per_s"])
+    return SM_COUNT * FP64_LANES_PER_SM * clock_ghz * 1e9
 
 
 def _census_expr(node, out: Counter, fns) -> None:
@@ -102,16 +116,28 @@ def fp64_ops(layout) -> int:
     return sum(FP64_COST.get(k, 1) * v for k, v in census(layout).items())
 
 
-def roofline(layout, hbm_gbs: float = 6539.2, clock_ghz: float = 1.965, kernel: str = "step") -> dict:
+def hbm_peak_gbs() -> float:
+    """MEASURED_PEAKS.json hbm_gbs (driver-written copy bandwidth), else the
+    value recorded on this pool's B200s."""
+    import json
+
+    p = _ROOT / "MEASURED_PEAKS.json"
+    if p.is_file():
+        return float(json.loads(p.read_text())["hbm_gbs"])
+    return 6548.5
+
+
+def roofline(layout, hbm_gbs: float | None = None, clock_ghz: float = 1.965, kernel: str = "step") -> dict:
     """Per instance-step: bytes, FP64 ops, time at the HBM and FP64 roofs."""
     ir = from_layout(layout)
     p = CudaPrinter(ir)
     p.emit_unit()
     b = bytes_per_instance(p._abi, kernel)
     f = fp64_ops(ir)
-    fp64_rate = SM_COUNT * FP64_LANES_PER_SM * clock_ghz * 1e9
+    hbm_gbs = hbm_peak_gbs() if hbm_gbs is None else hbm_gbs
+    rate = fp64_rate(clock_ghz)
     t_hbm = b / (hbm_gbs * 1e9)
-    t_fp = f / fp64_rate
+    t_fp = f / rate
     return {
         "mechanism": ir.mechanism,
         "bytes_per_instance": b,
@@ -121,7 +147,7 @@ def roofline(layout, hbm_gbs: float = 6539.2, clock_ghz: float = 1.965, kernel: 
         "t_fp64_ns": t_fp * 1e9,
         "bound": "hbm" if t_hbm >= t_fp else "fp64",
         "fp64_per_byte": f / max(b, 1),
-        "ridge_fp64_per_byte": fp64_rate / (hbm_gbs * 1e9),
+        "ridge_fp64_per_byte": rate / (hbm_gbs * 1e9),
         "max_hbm_fraction_at_fp64_roof": min(1.0, t_hbm / t_fp) if t_fp > 0 else 1.0,
     }
 
@@ -169,7 +195,7 @@ def measured(layout, ncu_summary: dict, n_instances: int, options=None) -> dict:
         "algorithmic_bytes": b,
         "measured_dram_bytes": dram / n_instances,
         "kernel_us": us,
-        "hbm_fraction_algorithmic": b * n_instances / (us * 1e-6) / 6548.5e9,
+        "hbm_fraction_algorithmic": b * n_instances / (us * 1e-6) / (hbm_peak_gbs() * 1e9),
         "fp64_pipe_fraction": fp64_meas * n_instances / (us * 1e-6) / fp64_rate,
     }
 

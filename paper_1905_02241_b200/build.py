@@ -134,3 +134,39 @@ def build_many(layouts, options: CudaOptions | None = None, fmad: bool | None = 
     jobs = jobs or min(8, os.cpu_count() or 4)
     with ThreadPoolExecutor(jobs) as pool:
         return list(pool.map(lambda l: build_mechanism(l, options, fmad), layouts))
+
+
+class GroupBuild:
+    """Built population group (codegen_cuda.emit_group): library + member ABIs."""
+
+    def __init__(self, so_path: Path, cu_path: Path, symbol: str, abis, text: str):
+        self.so_path = so_path
+        self.cu_path = cu_path
+        self.symbol = symbol
+        self.abis = abis
+        self.text = text
+
+
+def build_group(name: str, chains, fmad: bool = False, force: bool = False) -> GroupBuild:
+    """emit_group + nvcc -> content-addressed shared object (same keying as
+    build_mechanism: generated text, portable flags, header digest)."""
+    from .codegen_cuda import _cname, emit_group
+
+    unit, abis = emit_group(name, chains)
+    flags = base_flags(fmad)
+    portable = [f for f in flags if not f.startswith("-I")]
+    key = hashlib.sha256((unit.text + "\0" + " ".join(portable) + "\0" + _headers_digest()).encode()).hexdigest()[:20]
+    out_dir = BUILD / "mech"
+    stem = f"group_{_cname(name)}-{key}"
+    so = out_dir / f"lib{stem}.so"
+    cu = out_dir / f"{stem}.cu"
+    with _lock:
+        key_lock = _key_locks.setdefault(key, threading.Lock())
+    with key_lock:
+        out_dir.mkdir(parents=True, exist_ok=True)
+        if force or not so.is_file():
+            cu.write_text(unit.text)
+            tmp = so.with_suffix(f".so.tmp{os.getpid()}.{threading.get_ident()}")
+            _run([nvcc_path(), *flags, str(cu), "-o", str(tmp)], out_dir / f"{stem}.log")
+            tmp.replace(so)
+    return GroupBuild(so, cu, _cname(name), abis, unit.text)

@@ -109,12 +109,18 @@ class ColumnShard:
 
     def __init__(self, spec: ColumnSpec, cell_lo: int, cell_hi: int, options_for=None,
                  concurrent_soma: bool = False, reset: bool = True, host: dict | None = None,
-                 runners: dict | None = None):
+                 runners: dict | None = None, grouped_soma: bool = False):
         """`concurrent_soma`: the one-per-cell soma populations run on their
         own streams (CaDynamics_E2 after Ca_HVA, whose ica it reads) without
         touching the shared nodes; one combine kernel then folds their
         currents into the soma rhs/d in LAUNCH_ORDER -- the same operations
-        in the same order as the sequential launches."""
+        in the same order as the sequential launches.
+        `grouped_soma` (implies the combine): the soma populations are ONE
+        launch (runner.PopulationGroup, chains NaTs2_t | K_Pst |
+        Ca_HVA -> CaDynamics_E2 | SKv3_1) on a side stream, concurrent with
+        Ih: per timestep 4 launches (Ih, soma group, combine, synapses)
+        instead of 8 -- what matters when a rank holds few cells (strong
+        scaling)."""
         from .runner import CudaRunner, NodeArrays
 
         self.spec = spec
@@ -153,7 +159,9 @@ class ColumnShard:
         ih = self.devs["Ih"].nodes
         self._assign_first = bool(reset) and ih.seg_unique == 1 and ih.n == self.nodes.n_nodes
         ih.assign = 1 if self._assign_first else 0
-        self.concurrent = bool(concurrent_soma) and all(self.devs[m].nodes.seg_unique == 1 for m in SOMA_MECHS)
+        self.grouped = bool(grouped_soma) and all(self.devs[m].nodes.seg_unique == 1 for m in SOMA_MECHS)
+        self.concurrent = (bool(concurrent_soma) or self.grouped) and all(
+            self.devs[m].nodes.seg_unique == 1 for m in SOMA_MECHS)
         if self.concurrent:
             from . import runtime as rt
 
@@ -168,6 +176,17 @@ class ColumnShard:
             k = len(self._soma_order)
             self._iptr = (C.c_void_p * k)(*[self.devs[m].ptr["i_acc"] for m in self._soma_order])
             self._gptr = (C.c_void_p * k)(*[self.devs[m].ptr["g_acc"] for m in self._soma_order])
+        if self.grouped:
+            from .runner import PopulationGroup
+
+            def member(m):
+                return (self.runners[m], self.devs[m])
+
+            chains = [[member(m)] for m in self._soma_order if m not in ("Ca_HVA", "cadyn")]
+            chains.insert(self._soma_order.index("Ca_HVA"), [member("Ca_HVA"), member("cadyn")])
+            self.group = PopulationGroup("soma", chains)
+            self._group_stream = rt.Stream()
+            self._group_done = rt.Event()
 
     @property
     def n_instances(self) -> int:
@@ -197,6 +216,26 @@ class ColumnShard:
         L = rt.lib()
         main = self.stream
         first = self.devs[self._soma_order[0]]
+        soma_at = min(LAUNCH_ORDER.index(m) for m in SOMA_MECHS)
+        if self.grouped:
+            side = self._group_stream
+            for _ in range(steps):
+                self._reset_nodes()
+                self._fork.record(main)
+                rt.stream_wait(side, self._fork)
+                self.group.launch(side, 1)
+                self._group_done.record(side)
+                for stem in LAUNCH_ORDER[:soma_at]:
+                    self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
+                rt.stream_wait(main, self._group_done)
+                nb = first.nodes
+                rt.check(L.nmodl_combine_unique(C.c_void_p(nb.node_rhs), C.c_void_p(nb.node_d),
+                                                C.c_void_p(nb.node_index), first.n, self._iptr, self._gptr,
+                                                len(self._soma_order), C.c_void_p(main.handle)), "combine_unique")
+                for stem in LAUNCH_ORDER[soma_at:]:
+                    if stem not in SOMA_MECHS:
+                        self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
+            return
         for _ in range(steps):
             self._reset_nodes()
             self._fork.record(main)
@@ -214,7 +253,6 @@ class ColumnShard:
                 self._join[m].record(side)
             # folds in LAUNCH_ORDER: the populations before the soma group,
             # the soma group (combine, in order), the populations after it
-            soma_at = min(LAUNCH_ORDER.index(m) for m in SOMA_MECHS)
             for stem in LAUNCH_ORDER[:soma_at]:
                 self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
             for m in self._soma_order:
@@ -230,6 +268,8 @@ class ColumnShard:
     def kernels_per_step(self) -> int:
         """Our kernels per timestep: one fused step per population, plus the
         soma combine in concurrent mode."""
+        if self.grouped:
+            return len(LAUNCH_ORDER) - len(SOMA_MECHS) + 2  # + soma group + combine
         return len(LAUNCH_ORDER) + (1 if self.concurrent else 0)
 
     def check(self) -> None:
@@ -257,7 +297,7 @@ class ColumnShard:
 
 def simulate_column(spec: ColumnSpec, steps: int, cell_lo: int = 0, cell_hi: int | None = None,
                     host: dict | None = None, options_for=None, runners: dict | None = None,
-                    reset: bool = True, concurrent_soma: bool = False):
+                    reset: bool = True, concurrent_soma: bool = False, grouped_soma: bool = False):
     """Public column call (configs[4]): upload the stores of cells
     [cell_lo, cell_hi) (`host`, e.g. from host_stores(), ideally pinned),
     build the shared node layout on the device, nrn_init, `steps` timesteps
@@ -269,7 +309,7 @@ def simulate_column(spec: ColumnSpec, steps: int, cell_lo: int = 0, cell_hi: int
     if host is None:
         host = host_stores(spec, cell_lo, cell_hi)
     shard = ColumnShard(spec, cell_lo, cell_hi, options_for, concurrent_soma=concurrent_soma, reset=reset,
-                        host=host, runners=runners)
+                        host=host, runners=runners, grouped_soma=grouped_soma)
     shard.launch(steps)
     shard.check()
     for stem in LAUNCH_ORDER:

@@ -719,6 +719,73 @@ def tile_nodes_for(offsets: np.ndarray, tile: int) -> np.ndarray:
     return bounds
 
 
+class PopulationGroup:
+    """Several node_index populations stepped by ONE launch (a population
+    group, codegen_cuda.emit_group): `chains` is a list of chains of
+    (CudaRunner, DeviceInstanceData); each chain owns a contiguous CTA range,
+    its members run in order over the same instance-to-thread map (a later
+    member reads what an earlier one wrote for the same instance: the
+    Ca_HVA ica -> CaDynamics_E2 coupling).  Members must be one-instance-
+    per-node populations (their node binding has seg_unique 1 or 2); each
+    keeps its own store, status word and build options, and runs the same
+    generated code as its standalone kernel, so results are bit-identical.
+    Errors are reported through the members' runners (`check`)."""
+
+    def __init__(self, name: str, chains):
+        from .build import build_group
+
+        self.name = name
+        self.chains = [list(ch) for ch in chains]
+        runners = [r for ch in self.chains for r, _ in ch]
+        if not runners:
+            raise ValueError("empty population group")
+        flags = {r.flags for r in runners}
+        if len(flags) != 1:
+            raise ValueError("population group members need one Jacobian mode")
+        self.flags = flags.pop()
+        self.device = runners[0].device
+        self.gb = build_group(name, [[(r.ir, r.options) for r, _ in ch] for ch in self.chains])
+        self.lib = C.CDLL(str(self.gb.so_path))
+        g = self.gb.symbol
+        fields = [(f"md{ci}_{mi}", r.Struct) for ci, ch in enumerate(self.chains) for mi, (r, _) in enumerate(ch)]
+        fields.append(("cta", C.c_longlong * (len(self.chains) + 1)))
+        self.Args = type(f"{g}_args", (C.Structure,), {"_fields_": fields})
+        size_fn = getattr(self.lib, f"{g}_args_size")
+        size_fn.restype = C.c_longlong
+        if size_fn() != C.sizeof(self.Args):
+            raise RuntimeError(f"ABI mismatch for group {g}: C {size_fn()} vs ctypes {C.sizeof(self.Args)}")
+        self.fn = getattr(self.lib, f"{g}_step_unique")
+        self.fn.restype = C.c_int
+        self.fn.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int]
+        self.block = runners[0].options.block
+
+    def args(self):
+        vals = []
+        cta = [0]
+        for ch in self.chains:
+            for r, dev in ch:
+                if dev.nodes is None or dev.nodes.seg_unique not in (1, 2):
+                    raise ValueError(f"{r.mb.symbol}: group members need a one-instance-per-node binding")
+                vals.append(r._struct(dev))
+            n = max(dev.n for _, dev in ch)
+            cta.append(cta[-1] + (n + self.block - 1) // self.block)
+        return self.Args(*vals, (C.c_longlong * len(cta))(*cta))
+
+    def launch(self, stream: "rt.Stream", steps: int = 1) -> None:
+        """Enqueue `steps` group launches on `stream` (no sync, no checks)."""
+        a = self.args()
+        for ch in self.chains:
+            for r, dev in ch:
+                dev.dirty |= r._writes["step_nodes"]
+        rt.set_device(self.device)
+        rt.check(self.fn(C.byref(a), int(steps), C.c_void_p(stream.handle), self.flags), f"launch group {self.name}")
+
+    def check(self) -> None:
+        for ch in self.chains:
+            for r, dev in ch:
+                r.check(dev)
+
+
 def simulate(layout, data, steps: int, jac_mode: str = "exact", on_step=None, runner: CudaRunner | None = None):
     """GPU twin of modlc.interp.simulate (interp.py:640-655): one upload,
     initialize, `steps` fused state+current launches, one download."""

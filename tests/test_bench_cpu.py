@@ -71,7 +71,7 @@ def test_roofline_object_has_hbm_and_fp64_fractions(monkeypatch):
     import bench
 
     monkeypatch.setattr(bench, "_traffic_record", lambda: {})
-    r = bench._roofline("k", 1e9, 1e9, 1.0, ["x"], 1965.0)
+    r = bench._roofline("k", 1e9, (1e9, "census"), 1.0, ["x"], 1965.0)
     assert r["unit"] == "GB/s" and abs(r["achieved"] - 1000.0) < 1e-6
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-12
     assert r["fp64"]["frac"] > 0 and r["bound"] in ("hbm", "fp64")

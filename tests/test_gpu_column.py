@@ -12,23 +12,24 @@ from parity import TOL, node_dev, parity
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("bench_options,concurrent", [(False, False), (True, False), (False, True), (True, True)])
+@pytest.mark.parametrize("bench_options,concurrent", [(False, False), (True, False), (False, True), (True, True),
+                                                      (False, "grouped"), (True, "grouped")])
 def test_small_column_matches_oracle(bench_options, concurrent):
     """Default builds, and the builds bench.py measures (bench.options_for:
     relaxed rate arithmetic, fast_redo, ... -- here in node_index mode with
-    shared nodes and the one-instance-per-node path)."""
+    shared nodes and the one-instance-per-node path); sequential, concurrent
+    soma populations, and the soma populations as one grouped launch."""
     from paper_1905_02241_b200.column import COUPLINGS, LAUNCH_ORDER, ColumnShard, ColumnSpec, load_irs, shard_layout
     from paper_1905_02241_b200.instance import init_range
 
     spec = ColumnSpec(n_cells=300, dend_per_cell=5, syn_per_cell=12, seed=7)
     steps = 100
+    grouped = concurrent == "grouped"
+    opts = None
     if bench_options:
-        from bench import options_for
-
-        shard = ColumnShard(spec, 0, spec.n_cells, options_for, concurrent_soma=concurrent)
-    else:
-        shard = ColumnShard(spec, 0, spec.n_cells, concurrent_soma=concurrent)
-    assert shard.concurrent == concurrent
+        from bench import options_for as opts
+    shard = ColumnShard(spec, 0, spec.n_cells, opts, concurrent_soma=bool(concurrent), grouped_soma=grouped)
+    assert shard.concurrent == bool(concurrent) and shard.grouped == grouped
     shard.launch(steps)
     shard.check()
     irs = load_irs()
@@ -72,16 +73,19 @@ def test_concurrent_soma_is_bit_identical_and_graph_capturable():
 
     spec = ColumnSpec(n_cells=700, dend_per_cell=6, syn_per_cell=9, seed=5)
     seq = ColumnShard(spec, 0, spec.n_cells)
-    con = ColumnShard(spec, 0, spec.n_cells, concurrent_soma=True)
     seq.launch(30)
-    g = rt.capture(con.stream, lambda: con.launch(30))
-    g.launch(con.stream)
     seq.check()
-    con.check()
-    a, b = seq.nodes.download(seq.stream), con.nodes.download(con.stream)
-    for k in ("node_rhs", "node_d"):
-        np.testing.assert_array_equal(a[k].view(np.int64), b[k].view(np.int64), err_msg=k)
-    np.testing.assert_array_equal(seq.checksums(), con.checksums())
+    a = seq.nodes.download(seq.stream)
+    for mode in ("concurrent", "grouped"):
+        con = ColumnShard(spec, 0, spec.n_cells, concurrent_soma=True, grouped_soma=mode == "grouped")
+        assert con.grouped == (mode == "grouped")
+        g = rt.capture(con.stream, lambda: con.launch(30))
+        g.launch(con.stream)
+        con.check()
+        b = con.nodes.download(con.stream)
+        for k in ("node_rhs", "node_d"):
+            np.testing.assert_array_equal(a[k].view(np.int64), b[k].view(np.int64), err_msg=f"{mode}: {k}")
+        np.testing.assert_array_equal(seq.checksums(), con.checksums(), err_msg=mode)
     assert set(LAUNCH_ORDER)
 
 

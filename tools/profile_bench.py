@@ -13,8 +13,8 @@ kernels (launch-skip over the warm-up).  The parent then
     (tools/ncu_summary.py: time, DRAM bytes, pipes, occupancy, stalls, opcode
     mix per kernel), and
   * records every captured kernel's DRAM bytes (read + write, one launch)
-    under its build key (the content-addressed library stem) in
-    OUT_DIR/ncu_traffic.json, which bench.py reads as `roofline.traffic`
+    under "<build key>@<instances>" (the content-addressed library stem and
+    the population size) in OUT_DIR/ncu_traffic.json, which bench.py reads as `roofline.traffic`
     when the build it times has the same key (copy it to profiles/).
 """
 
@@ -32,6 +32,7 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tools"))
 
 WARM = 3
+FP64_OPCODES = ("DFMA", "DMUL", "DADD", "DSETP", "DMNMX")  # the FP64 pipe (paper_1905_02241_b200.analysis)
 
 
 def child(workload: str, out: str) -> None:
@@ -45,7 +46,8 @@ def child(workload: str, out: str) -> None:
     if workload == "column":
         from paper_1905_02241_b200.column import LAUNCH_ORDER, ColumnShard
 
-        shard = ColumnShard(bench._column_spec(), 0, bench.WORKLOADS["column"]["cells"], bench.options_for,
+        spec = bench._column_spec()
+        shard = ColumnShard(spec, 0, spec.n_cells, bench.options_for,
                             concurrent_soma=True)
         shard.launch(WARM)
         shard.stream.sync()
@@ -96,6 +98,9 @@ def _num(v: str) -> float:
 def parent(out_dir: Path, workloads: list[str]) -> None:
     import bench
 
+    import os
+
+    tag = os.environ.get("PROFILE_TAG", out_dir.name)  # where the summaries get committed under profiles/
     out_dir.mkdir(parents=True, exist_ok=True)
     traffic_path = out_dir / "ncu_traffic.json"
     record = json.loads(traffic_path.read_text()) if traffic_path.is_file() else {"by_build": {}}
@@ -129,14 +134,26 @@ def parent(out_dir: Path, workloads: list[str]) -> None:
             if k is None:
                 continue
             dram = _num(r["dram__bytes_read.sum"]) + _num(r["dram__bytes_write.sum"])
-            record["by_build"][k["build"]] = {
+            record["by_build"][f"{k['build']}@{k['n']}"] = {
                 "kernel": name, "workload": wl, "instances": k["n"], "dram_bytes": dram,
                 "dram_read": _num(r["dram__bytes_read.sum"]), "dram_write": _num(r["dram__bytes_write.sum"]),
                 "us": _num(r["gpu__time_duration.sum"]) / 1e3, "bytes_per_launch": k.get("bytes_per_launch"),
-                "capture": f"profiles/{out_dir.name}/{wl}.ncu-rep (ncu --set full, one launch after {WARM} warm-up steps)",
+                "capture": f"ncu --set full, one launch after {WARM} warm-up steps; summary "
+                           f"profiles/{tag}/{wl}.json",
             }
         subprocess.run([sys.executable, str(ROOT / "tools" / "ncu_summary.py"), str(out_dir),
                         f"{rep}.ncu-rep"], check=False)
+        # measured FP64 pipe instructions per instance (opcode mix x 32 lanes / n)
+        summ = out_dir / f"{wl}.json"
+        if summ.is_file():
+            for e in json.loads(summ.read_text()):
+                name = e["kernel"].split("(")[0].split("<")[0].replace("void ", "").strip()
+                k = by_kernel.get(name)
+                ops = (e.get("instructions") or {}).get("by_opcode_per_instance") or {}
+                key = f"{k['build']}@{k['n']}" if k else None
+                if key in record["by_build"] and ops:
+                    fp = sum(v for op, v in ops.items() if op in FP64_OPCODES)
+                    record["by_build"][key]["fp64_instr_per_instance"] = 32.0 * fp / k["n"]
         traffic_path.write_text(json.dumps(record, indent=1, sort_keys=True) + "\n")
     print("wrote", traffic_path)
 

@@ -16,8 +16,6 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
-import ctypes as C  # noqa: E402
-
 from paper_1905_02241_b200 import runtime as rt  # noqa: E402
 from paper_1905_02241_b200.codegen_cuda import CudaOptions  # noqa: E402
 from paper_1905_02241_b200.instance import init, node_layout  # noqa: E402
@@ -44,23 +42,29 @@ def run(stem, opts, nodes=0, steps=30):
         kernel = "step_nodes"
     r.run_kernel(dev, "initialize", 1)
     info = rt.device_info(0)
-    lb = launch_bytes(r.abi, n, kernel, nodes)
-    flush = rt.DeviceBuffer(2 * info["l2_bytes"]) if lb < 3 * info["l2_bytes"] else None
-    a, b = rt.Event(), rt.Event()
+    lb = launch_bytes(r.abi, n, kernel, dev.nodes.n_segs if dev.nodes is not None else 0)
+    # bench.py's timing: one graph of `steps` launches, external events around
+    # each launch, the clean L2 flush between them for L2-sized stores
+    from bench import L2Flush
+
+    flush = L2Flush(info["l2_bytes"]) if lb < 3 * info["l2_bytes"] else None
     for _ in range(int(os.environ.get("TUNE_WARMUP", "10"))):
         r.launch(dev, kernel, 1)
     r.stream.sync()
-    total = 0.0
-    for _ in range(steps):
-        # head start: the host enqueues flush + events + launch before the GPU gets there
-        rt.check(rt.lib().nmodl_spin(1_000_000, C.c_void_p(r.stream.handle)), "spin")
-        if flush:
-            rt.check(rt.lib().nmodl_l2_flush(C.c_void_p(flush.ptr), flush.nbytes // 8, C.c_void_p(r.stream.handle)), "f")
-        a.record(r.stream)
-        r.launch(dev, kernel, 1)
-        b.record(r.stream)
-        b.sync()
-        total += a.elapsed_ms(b)
+    evs = [(rt.Event(), rt.Event()) for _ in range(steps)]
+
+    def body():
+        for a, b in evs:
+            if flush is not None:
+                flush(r.stream)
+            a.record_external(r.stream)
+            r.launch(dev, kernel, 1)
+            b.record_external(r.stream)
+
+    g = rt.capture(r.stream, body)
+    g.launch(r.stream)
+    r.stream.sync()
+    total = sum(a.elapsed_ms(b) for a, b in evs)
     r.check(dev)
     ms = total / steps
     return {"stem": stem, "opts": opts.__dict__ if hasattr(opts, "__dict__") else str(opts), "kernel": kernel, "n": n,

@@ -538,6 +538,15 @@ def _physical_gpu(device):
     return device
 
 
+def _column_mode():
+    """Launch schedule of the column step (NMODL_COLUMN_MODE, column.SCHEDULES):
+    "overlap" (default: Ih + the soma populations as one population-group
+    launch running concurrently with the synapse kernel, then one
+    node-ordered combine), "grouped", "concurrent" or "sequential" -- all
+    bit-identical (tests/test_gpu_column.py)."""
+    return {"schedule": os.environ.get("NMODL_COLUMN_MODE", "overlap")}
+
+
 def _column_spec():
     from paper_1905_02241_b200.column import ColumnSpec
 
@@ -553,8 +562,7 @@ def run_column(args, dist, sustained=True):
 
     spec = _column_spec()
     bounds = partition_cells(np.full(spec.n_cells, spec.cell_cost()), dist.world)
-    shard = ColumnShard(spec, int(bounds[dist.rank]), int(bounds[dist.rank + 1]), options_for,
-                        concurrent_soma=os.environ.get("NMODL_COLUMN_SEQUENTIAL") is None)
+    shard = ColumnShard(spec, int(bounds[dist.rank]), int(bounds[dist.rank + 1]), options_for, **_column_mode())
     s0 = shard.stream
     K, W = args.steps, args.warmup
     shard.launch(W)
@@ -611,10 +619,10 @@ def run_column(args, dist, sustained=True):
     table = dist.allgather(shard.checksums())
     from paper_1905_02241_b200.traffic import launch_bytes
 
-    keys = [f"{shard.runners[m].mb.so_path.stem[3:]}@{shard.devs[m].n}" for m in LAUNCH_ORDER]
-    parts = [_fp64_instr(shard.runners[m].ir, shard.devs[m].n, k) for m, k in zip(LAUNCH_ORDER, keys)]
+    keys, parts = _column_keys(shard)
     fp64 = (sum(p[0] for p in parts), "; ".join(sorted({p[1] for p in parts})))
-    roof = _roofline("7 x <mech>_k_step_nodes + soma combine (whole step)", shard.launch_bytes(), fp64, ms / K, keys,
+    roof = _roofline(f"whole step: {shard.kernels_per_step()} launches ({shard.schedule} schedule)",
+                     shard.launch_bytes(), fp64, ms / K, keys,
                      clocks.get("sm_mhz"))
     roof["share_of_step"] = 1.0
     per_mech = {}
@@ -638,10 +646,42 @@ def run_column(args, dist, sustained=True):
     }
 
 
+def _column_keys(shard):
+    """Build keys ("<library stem>@<instances>") of the kernels one column step
+    launches, and their FP64 instruction counts: the standalone population
+    kernels, or -- grouped soma mode -- Ih, the synapses and the soma group
+    (whose instance count is the sum of its members')."""
+    from paper_1905_02241_b200.column import LAUNCH_ORDER, SOMA_MECHS
+
+    keys, parts = [], []
+    for m in LAUNCH_ORDER:
+        if m in shard.group_members:
+            continue
+        k = f"{shard.runners[m].mb.so_path.stem[3:]}@{shard.devs[m].n}"
+        keys.append(k)
+        parts.append(_fp64_instr(shard.runners[m].ir, shard.devs[m].n, k))
+    if shard.grouped:
+        n = sum(shard.devs[m].n for m in shard.group_members)
+        k = f"{shard.group.gb.so_path.stem[3:]}@{n}"
+        keys.append(k)
+        e = _traffic_record().get("by_build", {}).get(k, {})
+        if "fp64_instr_per_instance" in e:
+            parts.append((e["fp64_instr_per_instance"] * n, "ncu-measured FP64 instructions of this build"))
+        else:
+            for m in shard.group_members:
+                parts.append(_fp64_instr(shard.runners[m].ir, shard.devs[m].n, "?"))
+    return keys, parts
+
+
 def C_void(x):
     import ctypes
 
     return ctypes.c_void_p(x)
+
+
+# simulate_nodes pipelines the upload of later instance chunks with the
+# stepping of earlier ones (bit-identical; tests/test_gpu_nodes.py)
+E2E_CHUNKS = int(os.environ.get("NMODL_E2E_CHUNKS", "4"))
 
 
 def e2e_measure(name, dist, calls=2, timesteps=1000):
@@ -676,9 +716,13 @@ def e2e_measure(name, dist, calls=2, timesteps=1000):
                 simulate(ir, data, timesteps, runner=runner)
             else:
                 t = {}
-                simulate_nodes(ir, data, timesteps, extra[0], extra[1], runner=runner, timings=t)
+                simulate_nodes(ir, data, timesteps, extra[0], extra[1], runner=runner, timings=t,
+                               chunks=E2E_CHUNKS)
                 for k, v in t.items():
-                    phases[k] = phases.get(k, 0.0) + v
+                    if isinstance(v, float):
+                        phases[k] = phases.get(k, 0.0) + v
+                    else:
+                        phases[k] = v
 
     one_call()  # warm-up (also primes graph/occupancy caches)
     phases.clear()
@@ -687,17 +731,18 @@ def e2e_measure(name, dist, calls=2, timesteps=1000):
     for _ in range(calls):
         one_call()
     dt = time.perf_counter() - t0
-    phases["unaccounted"] = dt - sum(phases.values())
+    phases["unaccounted"] = dt - sum(v for v in phases.values() if isinstance(v, float))
     dt = dist.allreduce([dt], "max")[0]
     n_all = dist.allreduce([float(sum(j[5] for j in jobs))], "sum")[0]
     h2d = int(sum(_h2d(j) for j in jobs))
     d2h = int(sum(_d2h(j) for j in jobs))
     return _e2e_line(n_all * timesteps * calls / dt, h2d, d2h, timesteps, calls,
                      f"one public-API call (runner.simulate{'_nodes' if w['nodes'] else ''}): pinned H2D of the store"
-                     + (", node_index + node_v upload, device sort" if w["nodes"] else "")
+                     + (f", node_index + node_v upload, device sort; {E2E_CHUNKS} instance chunks, upload of later "
+                        "chunks overlapped with stepping of earlier ones" if w["nodes"] else "")
                      + f", nrn_init, {timesteps} timesteps, D2H of the written arrays"
                      + (" and node rhs/d" if w["nodes"] else ""),
-                     {k: v / calls for k, v in phases.items()})
+                     {k: (v / calls if isinstance(v, float) else v) for k, v in phases.items()})
 
 
 def _e2e_line(value, h2d_call, d2h_call, timesteps, calls, step, phases=None):
@@ -752,9 +797,9 @@ def e2e_column(dist, calls=1, timesteps=1000):
     host = host_stores(spec, lo, hi)
     pins = [rt.PinnedRegistration(a) for h in host.values() for a in list(h.arrays.values()) + list(h.acc.values())]
     lay = shard_layout(spec, lo, hi)
-    conc = os.environ.get("NMODL_COLUMN_SEQUENTIAL") is None
+    mode = _column_mode()
     # warm-up call: loads the kernels (reused below), primes the caches
-    _, _, shard = simulate_column(spec, 10, lo, hi, host=host, options_for=options_for, concurrent_soma=conc)
+    _, _, shard = simulate_column(spec, 10, lo, hi, host=host, options_for=options_for, **mode)
     runners = shard.runners
     writes = {m: runners[m]._writes["initialize"] | runners[m]._writes["step_nodes"] | {"v"} for m in LAUNCH_ORDER}
     del shard
@@ -764,7 +809,7 @@ def e2e_column(dist, calls=1, timesteps=1000):
     t0 = time.perf_counter()
     for _ in range(calls):
         _, nodes, shard = simulate_column(spec, timesteps, lo, hi, host=host, options_for=options_for,
-                                          runners=runners, concurrent_soma=conc)
+                                          runners=runners, **mode)
     dt = time.perf_counter() - t0
     dt = dist.allreduce([dt], "max")[0]
     n_rank = sum(h.n for h in host.values())
@@ -921,6 +966,7 @@ def main():
     }
     if column:
         config["cells"] = _column_spec().n_cells
+        config["schedule"] = _column_mode()["schedule"]
     line = {"metric": METRIC, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "scaling": "strong" if column else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (modlc.interp.init-format seeded instance store; random node_index)",

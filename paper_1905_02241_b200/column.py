@@ -9,14 +9,17 @@ SPEC.md:441, modlc/layout.py:124-128).  Cell c owns compartments (nodes)
   soma + every dendrite:        Ih
   S synapses per cell:          ProbAMPANMDA_EMS on random compartments of the cell
 
-Per timestep the populations run in LAUNCH_ORDER, each one fused kernel that
-gathers v from the shared node voltage, runs nrn_state + nrn_cur and folds its
-currents into the shared node rhs/d in instance order.  The node rhs/d are
-rebuilt every timestep (a cable solver's matrix setup): Ih, which has one
-instance on every compartment, goes first and assigns them (rhs = 0 - i,
-d = 0 + g); the other populations accumulate.  CaDynamics_E2 reads
-Ca_HVA's `ica` array directly (ion coupling; Ca_HVA is launched first), which
-is what NEURON's shared ion arrays do.  Instance data are drawn with
+Per timestep every population runs one fused kernel that gathers v from the
+shared node voltage and runs nrn_state + nrn_cur; the currents are folded
+into the shared node rhs/d in LAUNCH_ORDER (synapses, Ih, the soma
+populations), each population in instance order.  The node rhs/d are rebuilt
+every timestep (a cable solver's matrix setup): they start from 0 and every
+population subtracts its currents (rhs) and adds its conductances (d).
+ColumnShard's schedules arrange the launches differently (one stream, side
+streams, one grouped launch, or the grouped launch overlapping the synapse
+kernel) but perform the same operations per node in the same order.
+CaDynamics_E2 reads Ca_HVA's `ica` array directly (ion coupling; Ca_HVA runs
+first), which is what NEURON's shared ion arrays do.  Instance data are drawn with
 `init_range`, so a shard of cells [lo, hi) holds exactly the instances the
 single-GPU column holds for those cells: shard checksums add up across ranks.
 """
@@ -34,7 +37,7 @@ from .ir import MechIR
 
 FIXTURES = Path(__file__).resolve().parent.parent / "fixtures" / "ir"
 SOMA_MECHS = ("NaTs2_t", "K_Pst", "Ca_HVA", "cadyn", "SKv3_1")
-LAUNCH_ORDER = ("Ih", "NaTs2_t", "K_Pst", "Ca_HVA", "cadyn", "SKv3_1", "ProbAMPANMDA_EMS")
+LAUNCH_ORDER = ("ProbAMPANMDA_EMS", "Ih", "NaTs2_t", "K_Pst", "Ca_HVA", "cadyn", "SKv3_1")
 COUPLINGS = (("cadyn", "ica", "Ca_HVA", "ica"),)  # consumer slot <- producer slot
 
 
@@ -104,25 +107,43 @@ def load_irs() -> dict:
     return {stem: MechIR.load(FIXTURES / f"{stem}.json") for stem in LAUNCH_ORDER}
 
 
+SCHEDULES = ("sequential", "concurrent", "grouped", "overlap")
+
+
 class ColumnShard:
-    """All populations of cells [cell_lo, cell_hi) resident on one GPU."""
+    """All populations of cells [cell_lo, cell_hi) resident on one GPU.
+
+    Per timestep every population runs once and folds its currents into the
+    shared node rhs/d in LAUNCH_ORDER (synapses, Ih, then the soma
+    populations; Ca_HVA before CaDynamics_E2, which reads its ica).  The
+    `schedule` only changes how the launches are arranged -- every schedule
+    performs the same operations on every node in the same order, so all
+    give bit-identical results (tests/test_gpu_column.py):
+
+    * "sequential": one launch per population on one stream;
+    * "concurrent": the one-per-cell soma populations on side streams,
+      leaving their currents in i_acc/g_acc (seg_unique 2); one combine
+      kernel folds them into the soma nodes in order;
+    * "grouped": the soma populations as ONE launch (runner.PopulationGroup,
+      chains NaTs2_t | K_Pst | Ca_HVA -> CaDynamics_E2 | SKv3_1) on a side
+      stream, then the combine;
+    * "overlap": Ih joins the group, so the whole per-instance work except
+      the synapses is one launch that runs CONCURRENTLY with the synapse
+      kernel (the synapses fold first, into the nodes they touch); one
+      node-ordered combine (nmodl_combine_nodes) then folds Ih and the soma
+      populations.  3 launches per timestep -- what matters when a rank
+      holds few cells (strong scaling)."""
 
     def __init__(self, spec: ColumnSpec, cell_lo: int, cell_hi: int, options_for=None,
                  concurrent_soma: bool = False, reset: bool = True, host: dict | None = None,
-                 runners: dict | None = None, grouped_soma: bool = False):
-        """`concurrent_soma`: the one-per-cell soma populations run on their
-        own streams (CaDynamics_E2 after Ca_HVA, whose ica it reads) without
-        touching the shared nodes; one combine kernel then folds their
-        currents into the soma rhs/d in LAUNCH_ORDER -- the same operations
-        in the same order as the sequential launches.
-        `grouped_soma` (implies the combine): the soma populations are ONE
-        launch (runner.PopulationGroup, chains NaTs2_t | K_Pst |
-        Ca_HVA -> CaDynamics_E2 | SKv3_1) on a side stream, concurrent with
-        Ih: per timestep 4 launches (Ih, soma group, combine, synapses)
-        instead of 8 -- what matters when a rank holds few cells (strong
-        scaling)."""
+                 runners: dict | None = None, grouped_soma: bool = False, schedule: str | None = None):
+        from . import runtime as rt
         from .runner import CudaRunner, NodeArrays
 
+        if schedule is None:
+            schedule = "grouped" if grouped_soma else ("concurrent" if concurrent_soma else "sequential")
+        if schedule not in SCHEDULES:
+            raise ValueError(f"schedule must be one of {SCHEDULES}")
         self.spec = spec
         self.reset = reset
         self.cells = (cell_lo, cell_hi)
@@ -154,28 +175,33 @@ class ColumnShard:
             self.runners[dst].share_slot(self.devs[dst], dslot, self.devs[src], sslot)
         for stem in LAUNCH_ORDER:
             self.runners[stem].run_kernel(self.devs[stem], "initialize", 1)
-        # per-step node reset: Ih (one instance per compartment, launched
-        # first) assigns rhs/d; otherwise a memset starts each step
-        ih = self.devs["Ih"].nodes
-        self._assign_first = bool(reset) and ih.seg_unique == 1 and ih.n == self.nodes.n_nodes
-        ih.assign = 1 if self._assign_first else 0
-        self.grouped = bool(grouped_soma) and all(self.devs[m].nodes.seg_unique == 1 for m in SOMA_MECHS)
-        self.concurrent = (bool(concurrent_soma) or self.grouped) and all(
-            self.devs[m].nodes.seg_unique == 1 for m in SOMA_MECHS)
-        if self.concurrent:
-            from . import runtime as rt
+        # per-step node reset: the first population assigns rhs/d when it has
+        # one instance on every node; otherwise a memset starts each step
+        fb = self.devs[LAUNCH_ORDER[0]].nodes
+        self._assign_first = bool(reset) and fb.seg_unique == 1 and fb.n == self.nodes.n_nodes
+        fb.assign = 1 if self._assign_first else 0
+        unique = all(self.devs[m].nodes.seg_unique == 1 for m in SOMA_MECHS)
+        if schedule != "sequential" and not unique:
+            schedule = "sequential"
+        if schedule == "overlap" and not (reset and self.devs["Ih"].nodes.seg_unique == 1):
+            schedule = "grouped"
+        self.schedule = schedule
+        self.grouped = schedule in ("grouped", "overlap")
+        self.concurrent = schedule != "sequential"
+        self._soma_order = [m for m in LAUNCH_ORDER if m in SOMA_MECHS]
+        import ctypes as C
 
-            self._side = {m: rt.Stream() for m in SOMA_MECHS}
-            self._fork, self._ca = rt.Event(), rt.Event()
-            self._join = {m: rt.Event() for m in SOMA_MECHS}
+        if self.concurrent:
+            self._fork = rt.Event()
             for m in SOMA_MECHS:
                 self.devs[m].nodes.seg_unique = 2  # currents stay in i_acc/g_acc
-            self._soma_order = [m for m in LAUNCH_ORDER if m in SOMA_MECHS]
-            import ctypes as C
-
             k = len(self._soma_order)
             self._iptr = (C.c_void_p * k)(*[self.devs[m].ptr["i_acc"] for m in self._soma_order])
             self._gptr = (C.c_void_p * k)(*[self.devs[m].ptr["g_acc"] for m in self._soma_order])
+        if schedule == "concurrent":
+            self._side = {m: rt.Stream() for m in SOMA_MECHS}
+            self._ca = rt.Event()
+            self._join = {m: rt.Event() for m in SOMA_MECHS}
         if self.grouped:
             from .runner import PopulationGroup
 
@@ -184,9 +210,48 @@ class ColumnShard:
 
             chains = [[member(m)] for m in self._soma_order if m not in ("Ca_HVA", "cadyn")]
             chains.insert(self._soma_order.index("Ca_HVA"), [member("Ca_HVA"), member("cadyn")])
-            self.group = PopulationGroup("soma", chains)
+            name = "soma"
+            if schedule == "overlap":
+                self.devs["Ih"].nodes.seg_unique = 2
+                chains.insert(0, [member("Ih")])
+                name = "cell"
+            self.group = PopulationGroup(name, chains)
             self._group_stream = rt.Stream()
             self._group_done = rt.Event()
+        if schedule == "overlap":
+            self._overlap_setup()
+
+    def _overlap_setup(self) -> None:
+        """Node maps of the node-ordered combine: which nodes the synapses
+        touched (their fold starts from the synapse sum, the others from 0),
+        the Ih instance of every node and the soma instance of the soma nodes
+        (positions in the node-sorted device stores)."""
+        from . import runtime as rt
+
+        nn = self.nodes.n_nodes
+        syn = self.node_index["ProbAMPANMDA_EMS"]
+        touched = (np.bincount(syn, minlength=nn) > 0).astype(np.uint8)
+
+        def inverse(idx):
+            srt = np.asarray(idx)[np.argsort(idx, kind="stable")]
+            out = np.full(nn, -1, dtype=np.int32)
+            out[srt] = np.arange(len(srt), dtype=np.int32)
+            return out
+
+        maps = [touched, inverse(self.node_index["Ih"]), inverse(self.node_index[self._soma_order[0]])]
+        self._maps = [rt.DeviceBuffer(max(m.nbytes, 8)) for m in maps]
+        for buf, m in zip(self._maps, maps):
+            rt.h2d(buf.ptr, m.ctypes.data, m.nbytes, self.stream)
+        self.stream.sync()
+        syn_nb = self.devs["ProbAMPANMDA_EMS"].nodes
+        syn_nb.assign = 1  # first fold of the step, into the nodes it touches
+
+    @property
+    def group_members(self) -> list[str]:
+        """Populations stepped inside the population-group launch."""
+        if not self.grouped:
+            return []
+        return [m for m in LAUNCH_ORDER if m in SOMA_MECHS or (m == "Ih" and self.schedule == "overlap")]
 
     @property
     def n_instances(self) -> int:
@@ -202,75 +267,83 @@ class ColumnShard:
             rt.memset(self.nodes.node_rhs, 0, nbytes, self.stream)
             rt.memset(self.nodes.node_d, 0, nbytes, self.stream)
 
+    def _combine_soma(self, L, C) -> None:
+        from . import runtime as rt
+
+        first = self.devs[self._soma_order[0]]
+        nb = first.nodes
+        rt.check(L.nmodl_combine_unique(C.c_void_p(nb.node_rhs), C.c_void_p(nb.node_d), C.c_void_p(nb.node_index),
+                                        first.n, self._iptr, self._gptr, len(self._soma_order),
+                                        C.c_void_p(self.stream.handle)), "combine_unique")
+
     def launch(self, steps: int = 1) -> None:
-        if not self.concurrent:
-            for _ in range(steps):
-                self._reset_nodes()
-                for stem in LAUNCH_ORDER:
-                    self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
-            return
         import ctypes as C
 
         from . import runtime as rt
 
         L = rt.lib()
         main = self.stream
-        first = self.devs[self._soma_order[0]]
         soma_at = min(LAUNCH_ORDER.index(m) for m in SOMA_MECHS)
-        if self.grouped:
-            side = self._group_stream
-            for _ in range(steps):
+        before = [m for m in LAUNCH_ORDER[:soma_at]]
+        after = [m for m in LAUNCH_ORDER[soma_at:] if m not in SOMA_MECHS]
+        for _ in range(steps):
+            if self.schedule == "sequential":
                 self._reset_nodes()
+                for stem in LAUNCH_ORDER:
+                    self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
+                continue
+            if self.schedule == "overlap":
+                side = self._group_stream
                 self._fork.record(main)
                 rt.stream_wait(side, self._fork)
                 self.group.launch(side, 1)
                 self._group_done.record(side)
-                for stem in LAUNCH_ORDER[:soma_at]:
-                    self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
+                syn = "ProbAMPANMDA_EMS"
+                self.runners[syn].launch(self.devs[syn], "step_nodes", 1)
                 rt.stream_wait(main, self._group_done)
-                nb = first.nodes
-                rt.check(L.nmodl_combine_unique(C.c_void_p(nb.node_rhs), C.c_void_p(nb.node_d),
-                                                C.c_void_p(nb.node_index), first.n, self._iptr, self._gptr,
-                                                len(self._soma_order), C.c_void_p(main.handle)), "combine_unique")
-                for stem in LAUNCH_ORDER[soma_at:]:
-                    if stem not in SOMA_MECHS:
-                        self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
-            return
-        for _ in range(steps):
+                ih, soma = self.devs["Ih"], self.devs[self._soma_order[0]]
+                rt.check(L.nmodl_combine_nodes(
+                    C.c_void_p(self.nodes.node_rhs), C.c_void_p(self.nodes.node_d), self.nodes.n_nodes,
+                    C.c_void_p(self._maps[0].ptr), C.c_void_p(self._maps[1].ptr), C.c_void_p(ih.ptr["i_acc"]),
+                    C.c_void_p(ih.ptr["g_acc"]), C.c_void_p(self._maps[2].ptr), self._iptr, self._gptr,
+                    len(self._soma_order), C.c_void_p(main.handle)), "combine_nodes")
+                continue
             self._reset_nodes()
             self._fork.record(main)
-            for m in self._soma_order:
-                side = self._side[m]
+            if self.schedule == "grouped":
+                side = self._group_stream
                 rt.stream_wait(side, self._fork)
-                if m == "cadyn":
-                    rt.stream_wait(side, self._ca)  # reads this step's Ca_HVA ica
-                r = self.runners[m]
-                r.stream = side
-                r.launch(self.devs[m], "step_nodes", 1)
-                r.stream = main
-                if m == "Ca_HVA":
-                    self._ca.record(side)
-                self._join[m].record(side)
+                self.group.launch(side, 1)
+                self._group_done.record(side)
+                joins = [self._group_done]
+            else:
+                for m in self._soma_order:
+                    side = self._side[m]
+                    rt.stream_wait(side, self._fork)
+                    if m == "cadyn":
+                        rt.stream_wait(side, self._ca)  # reads this step's Ca_HVA ica
+                    r = self.runners[m]
+                    r.stream = side
+                    r.launch(self.devs[m], "step_nodes", 1)
+                    r.stream = main
+                    if m == "Ca_HVA":
+                        self._ca.record(side)
+                    self._join[m].record(side)
+                joins = [self._join[m] for m in self._soma_order]
             # folds in LAUNCH_ORDER: the populations before the soma group,
             # the soma group (combine, in order), the populations after it
-            for stem in LAUNCH_ORDER[:soma_at]:
+            for stem in before:
                 self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
-            for m in self._soma_order:
-                rt.stream_wait(main, self._join[m])
-            nb = first.nodes
-            rt.check(L.nmodl_combine_unique(C.c_void_p(nb.node_rhs), C.c_void_p(nb.node_d), C.c_void_p(nb.node_index),
-                                            first.n, self._iptr, self._gptr, len(self._soma_order),
-                                            C.c_void_p(main.handle)), "combine_unique")
-            for stem in LAUNCH_ORDER[soma_at:]:
-                if stem not in SOMA_MECHS:
-                    self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
+            for e in joins:
+                rt.stream_wait(main, e)
+            self._combine_soma(L, C)
+            for stem in after:
+                self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
 
     def kernels_per_step(self) -> int:
-        """Our kernels per timestep: one fused step per population, plus the
-        soma combine in concurrent mode."""
-        if self.grouped:
-            return len(LAUNCH_ORDER) - len(SOMA_MECHS) + 2  # + soma group + combine
-        return len(LAUNCH_ORDER) + (1 if self.concurrent else 0)
+        """Our kernels per timestep (memsets not counted)."""
+        return {"sequential": len(LAUNCH_ORDER), "concurrent": len(LAUNCH_ORDER) + 1,
+                "grouped": len(LAUNCH_ORDER) - len(SOMA_MECHS) + 2, "overlap": 3}[self.schedule]
 
     def check(self) -> None:
         for stem in LAUNCH_ORDER:
@@ -297,7 +370,8 @@ class ColumnShard:
 
 def simulate_column(spec: ColumnSpec, steps: int, cell_lo: int = 0, cell_hi: int | None = None,
                     host: dict | None = None, options_for=None, runners: dict | None = None,
-                    reset: bool = True, concurrent_soma: bool = False, grouped_soma: bool = False):
+                    reset: bool = True, concurrent_soma: bool = False, grouped_soma: bool = False,
+                    schedule: str | None = None):
     """Public column call (configs[4]): upload the stores of cells
     [cell_lo, cell_hi) (`host`, e.g. from host_stores(), ideally pinned),
     build the shared node layout on the device, nrn_init, `steps` timesteps
@@ -309,7 +383,7 @@ def simulate_column(spec: ColumnSpec, steps: int, cell_lo: int = 0, cell_hi: int
     if host is None:
         host = host_stores(spec, cell_lo, cell_hi)
     shard = ColumnShard(spec, cell_lo, cell_hi, options_for, concurrent_soma=concurrent_soma, reset=reset,
-                        host=host, runners=runners, grouped_soma=grouped_soma)
+                        host=host, runners=runners, grouped_soma=grouped_soma, schedule=schedule)
     shard.launch(steps)
     shard.check()
     for stem in LAUNCH_ORDER:

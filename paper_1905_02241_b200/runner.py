@@ -195,10 +195,11 @@ class DeviceInstanceData:
         # never permuted, never downloaded
         self.unset: set[str] = set()
 
-    def reorder(self, perm_ptr: int, stream) -> None:
-        """new[k] = old[perm[k]] for every array, into a fresh arena."""
+    def reorder(self, perm_ptr: int, stream, arena: "rt.DeviceBuffer | None" = None, sync: bool = True) -> None:
+        """new[k] = old[perm[k]] for every array, into a fresh arena (or the
+        preallocated `arena`; `sync=False` leaves the permutes enqueued)."""
         names = list(self.names) + ["i_acc", "g_acc"]
-        arena = rt.DeviceBuffer(self.stride * len(names))
+        arena = arena or rt.DeviceBuffer(self.stride * len(names))
         L = rt.lib()
         new_ptr = {}
         for i, name in enumerate(names):
@@ -207,7 +208,9 @@ class DeviceInstanceData:
                 rt.check(L.nmodl_permute(C.c_void_p(self.ptr[name]), C.c_void_p(dst), C.c_void_p(perm_ptr), self.n,
                                          0, C.c_void_p(stream.handle)), "permute")
             new_ptr[name] = dst
-        stream.sync()
+        if sync:
+            stream.sync()
+        self.arena_prev = None if sync else self.arena  # keep the source alive until the permutes ran
         self.arena = arena  # the old arena returns to the allocator cache
         self.ptr = new_ptr
 
@@ -536,6 +539,22 @@ class CudaRunner:
                 raise ValueError("prepared node layout is for another population size")
         return self._finish_nodes(dev, nb)
 
+    def node_tile(self, n: int) -> int:
+        """Target instances per node tile: whole waves of the node kernel's
+        persistent grid (G resident CTAs, each looping over tiles) with at
+        most ~94% of the shared-memory tile, so every CTA gets the same
+        number of equal tiles (an unbalanced last wave costs up to a tile's
+        time; 1.25M synapses: 724 tiles on 592 CTAs took 1.6x as long)."""
+        if getattr(self, "_node_ctas", None) is None:
+            fn = getattr(self.lib, f"{self.mb.symbol}_step_nodes_ctas")
+            fn.restype = C.c_int
+            rt.set_device(self.device)
+            self._node_ctas = max(1, int(fn()))
+        G = self._node_ctas
+        cap = max(64, (15 * self.options.tile) // 16)
+        waves = max(1, -(-n // (G * cap)))
+        return max(64, -(-n // (G * waves)))
+
     def aux_stream(self) -> "rt.Stream":
         """A second stream of this runner (node layout built beside the upload)."""
         if getattr(self, "_aux", None) is None:
@@ -600,8 +619,7 @@ class CudaRunner:
         # Both are built on the device (nmodl_node_segments; host
         # restatement: tile_nodes_for) -- only two counts come back.
         if tile is None:
-            sms = rt.device_info(self.device)["sm_count"]
-            T = max(64, min((3 * self.options.tile) // 4, -(-n // (4 * sms))))
+            T = self.node_tile(n)
         else:
             T = int(tile)
         n_marks = -(-max(n, 1) // T)
@@ -615,22 +633,30 @@ class CudaRunner:
         nb._pending = (counts, bad)
         return nb
 
-    def _finish_nodes(self, dev: DeviceInstanceData, nb: NodeBinding) -> NodeBinding:
+    @staticmethod
+    def _enqueue_counts(nb: NodeBinding) -> None:
+        """Copy the layout's two counts and the range flag to the host (async)."""
         counts, bad = nb._pending
-        n = nb.n
-        s = nb.stream
-        cnt = np.empty(2, dtype=np.int64)
-        b = np.empty(1, dtype=np.int32)
-        rt.d2h(cnt.ctypes.data, counts, 16, s)
-        rt.d2h(b.ctypes.data, bad, 4, s)
-        s.sync()
+        nb._cnt = np.empty(2, dtype=np.int64)
+        nb._bad = np.empty(1, dtype=np.int32)
+        rt.d2h(nb._cnt.ctypes.data, counts, 16, nb.stream)
+        rt.d2h(nb._bad.ctypes.data, bad, 4, nb.stream)
+
+    def _apply_counts(self, nb: NodeBinding) -> None:
+        """After the counts landed: segment / tile counts, one-per-node flag."""
         nb._host_keep = None
-        s = nb.stream = self.stream
-        if b[0] != 0x7FFFFFFF:
-            raise ValueError(f"node_index out of range at instance {int(b[0])}")
-        nb.n_segs = int(cnt[0])
-        nb.n_tiles = int(cnt[1]) - 1
-        nb.seg_unique = 1 if nb.n_segs == n else 0  # every occupied node holds exactly one instance
+        nb.stream = self.stream
+        if nb._bad[0] != 0x7FFFFFFF:
+            raise ValueError(f"node_index out of range at instance {int(nb._bad[0])}")
+        nb.n_segs = int(nb._cnt[0])
+        nb.n_tiles = int(nb._cnt[1]) - 1
+        nb.seg_unique = 1 if nb.n_segs == nb.n else 0  # every occupied node holds exactly one instance
+
+    def _finish_nodes(self, dev: DeviceInstanceData, nb: NodeBinding) -> NodeBinding:
+        self._enqueue_counts(nb)
+        nb.stream.sync()
+        self._apply_counts(nb)
+        s = nb.stream
         self._mark("bind:segments_tiles")
         # reorder every instance array into node-sorted order (on the device):
         # gather into a fresh arena, then retire the old one (no copy back)
@@ -807,9 +833,125 @@ def simulate(layout, data, steps: int, jac_mode: str = "exact", on_step=None, ru
     return data
 
 
+class _NotChunkable(Exception):
+    """The pipelined path declines (inputs or mechanism outside its scope, or a
+    reported error): the caller runs the one-store path, which reproduces the
+    reference's error semantics exactly.  The host data is still untouched."""
+
+
+def _simulate_nodes_chunked(runner: "CudaRunner", data, steps: int, node_index, node_v, chunks: int, t: dict):
+    """simulate_nodes with the store split into `chunks` contiguous instance
+    ranges, pipelined: every device buffer is allocated and every chunk's
+    node layout sorted first (one host sync), then all H2D copies are
+    enqueued on a second stream, and each chunk is reordered, initialised
+    and stepped on the runner's stream as soon as its copy has landed -- the
+    PCIe upload of the later chunks overlaps the stepping of the earlier
+    ones, with no host sync (no cudaMalloc) until the end.
+
+    Same results, bit for bit, as the one-store path: instances are
+    independent and their voltage is the (constant) node voltage, so a chunk
+    can run all its steps before the next one starts; the node rhs/d of the
+    last step are the in-order folds over all instances, and chunk k's
+    instances follow chunk k-1's in instance order, so chunk 0 assigns the
+    touched nodes (0 - sum) and every later chunk accumulates onto them --
+    the same sequence of roundings as one fold.  The earlier steps fold into
+    scratch node arrays (their rhs/d are overwritten by the next step in the
+    one-store path too).  Any reported error (or a non-finite input) makes it
+    decline before anything was written back (_NotChunkable)."""
+    import time
+
+    clock = time.perf_counter
+    n = int(data.n)
+    if runner.n_newton or runner.abi.rw_scalars or steps < 1 or not np.isfinite(node_v).all():
+        raise _NotChunkable()
+    for a in list(data.arrays.values()) + list(data.acc.values()):
+        if not (a.flags.c_contiguous and a.dtype == np.float64):
+            raise _NotChunkable()
+    t0 = clock()
+    names = list(data.arrays)
+    up = runner.aux_stream()
+    s = runner.stream
+    L = rt.lib()
+    shared = NodeArrays(node_v, stream=s)
+    scratch = [rt.DeviceBuffer(8 * shared.n_nodes) for _ in range(2)]
+    bounds = [n * k // chunks for k in range(chunks + 1)]
+    parts = []
+    for k in range(chunks):  # every allocation and every node sort, up front
+        lo, hi = bounds[k], bounds[k + 1]
+        view = HostInstanceData(hi - lo, {m: a[lo:hi] for m, a in data.arrays.items()},
+                                {m: a[lo:hi] for m, a in data.acc.items()}, data.scalars)
+        dev = DeviceInstanceData(runner, hi - lo, names, data.scalars)
+        dev.unset |= {"v", "i_acc", "g_acc"}
+        nb = runner.prepare_nodes(hi - lo, node_index[lo:hi], shared=shared, stream=s)
+        runner._enqueue_counts(nb)
+        parts.append({"dev": dev, "view": view, "nb": nb, "lo": lo, "hi": hi,
+                      "arena": rt.DeviceBuffer(dev.stride * (len(names) + 2)),
+                      "scan": rt.DeviceBuffer(8 * len(names)), "landed": rt.Event()})
+    s.sync()
+    for p in parts:
+        runner._apply_counts(p["nb"])
+    t["layout"] = clock() - t0
+    t0 = clock()
+    ev0 = rt.Event()
+    ev0.record(up)
+    for p in parts:  # the uploads, all enqueued now on the second stream
+        dev, view = p["dev"], p["view"]
+        for m in names:
+            if m != "v":
+                rt.h2d(dev.ptr[m], view.arrays[m].ctypes.data, view.arrays[m].nbytes, up)
+        p["landed"].record(up)
+    for k, p in enumerate(parts):
+        dev, nb = p["dev"], p["nb"]
+        rt.stream_wait(s, p["landed"])
+        p["c0"], p["c1"] = rt.Event(), rt.Event()
+        p["c0"].record(s)
+        rt.memset(p["scan"].ptr, 0xFF, p["scan"].nbytes, s)
+        for i, m in enumerate(names):
+            if m != "v":
+                rt.check(L.nmodl_first_nonfinite(C.c_void_p(dev.ptr[m]), dev.n, C.c_void_p(p["scan"].ptr + 8 * i),
+                                                 C.c_void_p(s.handle)), "first_nonfinite")
+        dev.reorder(nb.perm, s, arena=p["arena"], sync=False)
+        dev.nodes = nb
+        runner.gather_voltage(dev)
+        runner.launch(dev, "initialize", 1)
+        nb.node_rhs, nb.node_d, nb.assign = scratch[0].ptr, scratch[1].ptr, 1
+        if steps > 1:
+            runner.launch(dev, "step_nodes", steps - 1)
+        nb.node_rhs, nb.node_d, nb.assign = shared.node_rhs, shared.node_d, (1 if k == 0 else 0)
+        runner.launch(dev, "step_nodes", 1)
+        p["c1"].record(s)
+    s.sync()
+    t["steps"] = clock() - t0
+    # device timeline (ms from the first upload): upload landed, chunk start / end
+    t["timeline_ms"] = [(round(ev0.elapsed_ms(p["landed"]), 3), round(ev0.elapsed_ms(p["c0"]), 3),
+                         round(ev0.elapsed_ms(p["c1"]), 3)) for p in parts]
+    for p in parts:
+        p["dev"].arena_prev = None
+        scan = np.empty(len(names), dtype=np.uint64)
+        rt.d2h(scan.ctypes.data, p["scan"].ptr, scan.nbytes, s)
+        s.sync()
+        if any(v != np.uint64(rt.NO_ERROR) for m, v in zip(names, scan) if m != "v"):
+            raise _NotChunkable()
+    st = runner._read_status()
+    if st.err_key != rt.NO_ERROR:
+        runner._reset_status()
+        raise _NotChunkable()
+    t0 = clock()
+    for p in parts:
+        runner.to_host(p["dev"], p["view"], only_dirty=True)
+    out = {}
+    for name in ("node_rhs", "node_d"):
+        arr = np.empty(shared.n_nodes)
+        rt.d2h(arr.ctypes.data, getattr(shared, name), arr.nbytes, s)
+        out[name] = arr
+    s.sync()
+    t["download"] = clock() - t0
+    return data, out["node_rhs"], out["node_d"]
+
+
 def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, node_d=None,
                    jac_mode: str = "exact", runner: CudaRunner | None = None, timings: dict | None = None,
-                   reset: bool = True):
+                   reset: bool = True, chunks: int = 1):
     """node_index run of one mechanism population (builder extension).
 
     Per timestep: v_i = node_v[node_index[i]]; nrn_state; nrn_cur; then
@@ -820,6 +962,8 @@ def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, 
     start from node_rhs/node_d and accumulate across steps instead.
     Instances are initialised with the gathered voltage.  Returns (data,
     node_rhs, node_d); `data` is updated in place in instance order.
+    `chunks` > 1 pipelines the host->device upload with the stepping
+    (_simulate_nodes_chunked; identical results; per-step reset only).
     `timings` (optional dict) receives wall-clock seconds per phase.
     """
     import time
@@ -829,6 +973,16 @@ def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, 
     t0 = clock()
     runner = runner or CudaRunner(layout, jac_mode=jac_mode)
     node_v = np.ascontiguousarray(node_v, dtype=np.float64)
+    if chunks > 1 and reset and node_rhs is None and node_d is None and int(data.n) >= 1024 * chunks:
+        try:
+            out = _simulate_nodes_chunked(runner, data, steps, np.ascontiguousarray(node_index, dtype=np.int32),
+                                          node_v, int(chunks), t)
+            if timings is not None:
+                timings.update(t)
+            return out
+        except _NotChunkable:
+            t = {}
+            t0 = clock()
     # the node layout (node_index upload, stable sort, segments, tiles) is
     # built on a second stream while the instance store uploads
     aux = runner.aux_stream()

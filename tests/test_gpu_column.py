@@ -12,24 +12,24 @@ from parity import TOL, node_dev, parity
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("bench_options,concurrent", [(False, False), (True, False), (False, True), (True, True),
-                                                      (False, "grouped"), (True, "grouped")])
-def test_small_column_matches_oracle(bench_options, concurrent):
+@pytest.mark.parametrize("bench_options", [False, True])
+@pytest.mark.parametrize("schedule", ["sequential", "concurrent", "grouped", "overlap"])
+def test_small_column_matches_oracle(bench_options, schedule):
     """Default builds, and the builds bench.py measures (bench.options_for:
     relaxed rate arithmetic, fast_redo, ... -- here in node_index mode with
-    shared nodes and the one-instance-per-node path); sequential, concurrent
-    soma populations, and the soma populations as one grouped launch."""
+    shared nodes and the one-instance-per-node path); every launch schedule
+    (one stream, concurrent soma populations, the soma populations as one
+    grouped launch, Ih + soma group overlapping the synapse kernel)."""
     from paper_1905_02241_b200.column import COUPLINGS, LAUNCH_ORDER, ColumnShard, ColumnSpec, load_irs, shard_layout
     from paper_1905_02241_b200.instance import init_range
 
     spec = ColumnSpec(n_cells=300, dend_per_cell=5, syn_per_cell=12, seed=7)
     steps = 100
-    grouped = concurrent == "grouped"
     opts = None
     if bench_options:
         from bench import options_for as opts
-    shard = ColumnShard(spec, 0, spec.n_cells, opts, concurrent_soma=bool(concurrent), grouped_soma=grouped)
-    assert shard.concurrent == bool(concurrent) and shard.grouped == grouped
+    shard = ColumnShard(spec, 0, spec.n_cells, opts, schedule=schedule)
+    assert shard.schedule == schedule
     shard.launch(steps)
     shard.check()
     irs = load_irs()
@@ -65,9 +65,11 @@ def test_column_shards_add_up():
 
 
 def test_concurrent_soma_is_bit_identical_and_graph_capturable():
-    """The concurrent soma schedule (side streams + in-order combine) gives
-    the sequential schedule's node rhs/d and states BIT FOR BIT, also when
-    the step is captured into a CUDA graph (as bench.py does)."""
+    """Every concurrent schedule (side streams + in-order combine; one
+    grouped soma launch; Ih + soma group overlapping the synapse kernel +
+    node-ordered combine) gives the sequential schedule's node rhs/d and
+    states BIT FOR BIT, also when the step is captured into a CUDA graph (as
+    bench.py does)."""
     from paper_1905_02241_b200 import runtime as rt
     from paper_1905_02241_b200.column import LAUNCH_ORDER, ColumnShard, ColumnSpec
 
@@ -76,9 +78,9 @@ def test_concurrent_soma_is_bit_identical_and_graph_capturable():
     seq.launch(30)
     seq.check()
     a = seq.nodes.download(seq.stream)
-    for mode in ("concurrent", "grouped"):
-        con = ColumnShard(spec, 0, spec.n_cells, concurrent_soma=True, grouped_soma=mode == "grouped")
-        assert con.grouped == (mode == "grouped")
+    for mode in ("concurrent", "grouped", "overlap"):
+        con = ColumnShard(spec, 0, spec.n_cells, schedule=mode)
+        assert con.schedule == mode
         g = rt.capture(con.stream, lambda: con.launch(30))
         g.launch(con.stream)
         con.check()

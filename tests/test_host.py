@@ -158,6 +158,34 @@ def test_mechanism_library_exports_and_abi(stem):
     assert size() == ctypes.sizeof(type("S", (ctypes.Structure,), {"_fields_": fields}))
 
 
+def test_population_group_builds_and_mirrors_member_structs():
+    """emit_group: one library whose args struct is the members' C-ABI
+    stores back to back plus the chain CTA ranges (mirrored by
+    runner.PopulationGroup); the member code is the standalone node
+    kernel's, namespaced; members with Newton solves are rejected."""
+    from paper_1905_02241_b200.build import build_group
+    from paper_1905_02241_b200.codegen_cuda import UnsupportedConstruct, emit_group
+
+    def struct_of(abi):
+        fields = [(x.name, {"i64": ctypes.c_longlong, "f64": ctypes.c_double}.get(x.ctype, ctypes.c_void_p))
+                  for x in abi.fields]
+        return type("S", (ctypes.Structure,), {"_fields_": fields})
+
+    chains = [[(load_ir("NaTs2_t"), None)], [(load_ir("Ca_HVA"), None), (load_ir("cadyn"), None)]]
+    gb = build_group("t_grp", chains)
+    assert gb.text == emit_group("t_grp", chains)[0].text  # deterministic
+    assert "t_grp_m1_1::CaDynamics_E2_k_step_nodes_unique" in gb.text
+    lib = ctypes.CDLL(str(gb.so_path))
+    assert hasattr(lib, "t_grp_step_unique")
+    size = lib.t_grp_args_size
+    size.restype = ctypes.c_longlong
+    fields = [(f"md{ci}_{mi}", struct_of(a)) for ci, row in enumerate(gb.abis) for mi, a in enumerate(row)]
+    fields.append(("cta", ctypes.c_longlong * 3))
+    assert size() == ctypes.sizeof(type("A", (ctypes.Structure,), {"_fields_": fields}))
+    with pytest.raises(UnsupportedConstruct):
+        emit_group("bad", [[(load_ir("cdp5ish"), None)]])
+
+
 def test_runner_fails_loudly_without_device():
     from paper_1905_02241_b200 import runtime as rt
 

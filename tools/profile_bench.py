@@ -47,17 +47,24 @@ def child(workload: str, out: str) -> None:
         from paper_1905_02241_b200.column import LAUNCH_ORDER, ColumnShard
 
         spec = bench._column_spec()
-        shard = ColumnShard(spec, 0, spec.n_cells, bench.options_for,
-                            concurrent_soma=True)
+        shard = ColumnShard(spec, 0, spec.n_cells, bench.options_for, **bench._column_mode())
         shard.launch(WARM)
         shard.stream.sync()
         shard.launch(1)
         shard.stream.sync()
         shard.check()
         per_step = shard.kernels_per_step()
+        from paper_1905_02241_b200.column import SOMA_MECHS
+
         for m in LAUNCH_ORDER:
+            if m in shard.group_members:
+                continue
             r, d = shard.runners[m], shard.devs[m]
             rows.append({"kernel": f"{r.mb.symbol}_k_step_nodes", "build": r.mb.so_path.stem[3:], "n": d.n})
+        if shard.grouped:
+            gb = shard.group.gb
+            rows.append({"kernel": f"{gb.symbol}_k_step_unique", "build": gb.so_path.stem[3:],
+                         "n": sum(shard.devs[m].n for m in shard.group_members)})
     else:
         w = bench.WORKLOADS[workload]
         dist = argparse.Namespace(rank=0)
@@ -109,9 +116,7 @@ def parent(out_dir: Path, workloads: list[str]) -> None:
         # the per-step kernel count is known after setup; a dry child run is
         # cheap compared to the capture, so read it from bench's own tables
         if wl == "column":
-            from paper_1905_02241_b200.column import LAUNCH_ORDER
-
-            per_step = len(LAUNCH_ORDER) + 1
+            per_step = {"sequential": 7, "concurrent": 8, "grouped": 4, "overlap": 3}[bench._column_mode()["schedule"]]
             regex = "regex:_k_step|combine"
         else:
             per_step = len(bench.WORKLOADS[wl]["mechs"])

@@ -540,11 +540,10 @@ def _physical_gpu(device):
 
 def _column_mode():
     """Launch schedule of the column step (NMODL_COLUMN_MODE, column.SCHEDULES):
-    "overlap" (default: Ih + the soma populations as one population-group
-    launch running concurrently with the synapse kernel, then one
-    node-ordered combine), "grouped", "concurrent" or "sequential" -- all
-    bit-identical (tests/test_gpu_column.py)."""
-    return {"schedule": os.environ.get("NMODL_COLUMN_MODE", "overlap")}
+    "grouped" (default: the soma populations as one population-group launch
+    beside Ih, then the in-order combine), "concurrent" or "sequential" --
+    all bit-identical (tests/test_gpu_column.py)."""
+    return {"schedule": os.environ.get("NMODL_COLUMN_MODE", "grouped")}
 
 
 def _column_spec():
@@ -679,11 +678,6 @@ def C_void(x):
     return ctypes.c_void_p(x)
 
 
-# simulate_nodes pipelines the upload of later instance chunks with the
-# stepping of earlier ones (bit-identical; tests/test_gpu_nodes.py)
-E2E_CHUNKS = int(os.environ.get("NMODL_E2E_CHUNKS", "4"))
-
-
 def e2e_measure(name, dist, calls=2, timesteps=1000):
     """Same metric through the public API with host buffers: each call uploads
     the population from pinned host memory, binds nodes, runs nrn_init and
@@ -716,8 +710,7 @@ def e2e_measure(name, dist, calls=2, timesteps=1000):
                 simulate(ir, data, timesteps, runner=runner)
             else:
                 t = {}
-                simulate_nodes(ir, data, timesteps, extra[0], extra[1], runner=runner, timings=t,
-                               chunks=E2E_CHUNKS)
+                simulate_nodes(ir, data, timesteps, extra[0], extra[1], runner=runner, timings=t)
                 for k, v in t.items():
                     if isinstance(v, float):
                         phases[k] = phases.get(k, 0.0) + v
@@ -738,8 +731,7 @@ def e2e_measure(name, dist, calls=2, timesteps=1000):
     d2h = int(sum(_d2h(j) for j in jobs))
     return _e2e_line(n_all * timesteps * calls / dt, h2d, d2h, timesteps, calls,
                      f"one public-API call (runner.simulate{'_nodes' if w['nodes'] else ''}): pinned H2D of the store"
-                     + (f", node_index + node_v upload, device sort; {E2E_CHUNKS} instance chunks, upload of later "
-                        "chunks overlapped with stepping of earlier ones" if w["nodes"] else "")
+                     + (", node_index + node_v upload, device sort" if w["nodes"] else "")
                      + f", nrn_init, {timesteps} timesteps, D2H of the written arrays"
                      + (" and node rhs/d" if w["nodes"] else ""),
                      {k: (v / calls if isinstance(v, float) else v) for k, v in phases.items()})

@@ -93,14 +93,6 @@ int nmodl_event_record_external(nmodl_event_t e, nmodl_stream_t s);
  * population order: rhs[node_index[j]] -= i_p[j], d[...] += g_p[j] */
 int nmodl_combine_unique(double *rhs, double *d, const int *node_index, long long n,
                          const double *const *i_ptrs, const double *const *g_ptrs, int n_pops, nmodl_stream_t s);
-/* node-ordered fold, thread per node j: start from rhs/d[j] where base_valid[j]
- * (an earlier kernel folded into the node) else 0; subtract/add the current of
- * the population on node j (first_of_node[j] >= 0: its instance index), then
- * those of up to 8 populations sharing second_of_node[j], in order */
-int nmodl_combine_nodes(double *rhs, double *d, long long n_nodes, const unsigned char *base_valid,
-                        const int *first_of_node, const double *i_first, const double *g_first,
-                        const int *second_of_node, const double *const *i_ptrs, const double *const *g_ptrs,
-                        int n_pops, nmodl_stream_t s);
 int nmodl_event_sync(nmodl_event_t e);
 int nmodl_event_elapsed_ms(nmodl_event_t a, nmodl_event_t b, float *ms);
 /* CUDA-graph capture of the per-timestep launch loop */

@@ -11,13 +11,13 @@ SPEC.md:441, modlc/layout.py:124-128).  Cell c owns compartments (nodes)
 
 Per timestep every population runs one fused kernel that gathers v from the
 shared node voltage and runs nrn_state + nrn_cur; the currents are folded
-into the shared node rhs/d in LAUNCH_ORDER (synapses, Ih, the soma
-populations), each population in instance order.  The node rhs/d are rebuilt
-every timestep (a cable solver's matrix setup): they start from 0 and every
-population subtracts its currents (rhs) and adds its conductances (d).
-ColumnShard's schedules arrange the launches differently (one stream, side
-streams, one grouped launch, or the grouped launch overlapping the synapse
-kernel) but perform the same operations per node in the same order.
+into the shared node rhs/d in LAUNCH_ORDER (Ih, the soma populations, the
+synapses), each population in instance order.  The node rhs/d are rebuilt
+every timestep (a cable solver's matrix setup): Ih, which has one instance
+on every compartment, goes first and assigns them (rhs = 0 - i, d = 0 + g);
+the other populations accumulate.  ColumnShard's schedules arrange the
+launches differently (one stream, side streams, one grouped launch) but
+perform the same operations per node in the same order.
 CaDynamics_E2 reads Ca_HVA's `ica` array directly (ion coupling; Ca_HVA runs
 first), which is what NEURON's shared ion arrays do.  Instance data are drawn with
 `init_range`, so a shard of cells [lo, hi) holds exactly the instances the
@@ -37,7 +37,7 @@ from .ir import MechIR
 
 FIXTURES = Path(__file__).resolve().parent.parent / "fixtures" / "ir"
 SOMA_MECHS = ("NaTs2_t", "K_Pst", "Ca_HVA", "cadyn", "SKv3_1")
-LAUNCH_ORDER = ("ProbAMPANMDA_EMS", "Ih", "NaTs2_t", "K_Pst", "Ca_HVA", "cadyn", "SKv3_1")
+LAUNCH_ORDER = ("Ih", "NaTs2_t", "K_Pst", "Ca_HVA", "cadyn", "SKv3_1", "ProbAMPANMDA_EMS")
 COUPLINGS = (("cadyn", "ica", "Ca_HVA", "ica"),)  # consumer slot <- producer slot
 
 
@@ -107,15 +107,15 @@ def load_irs() -> dict:
     return {stem: MechIR.load(FIXTURES / f"{stem}.json") for stem in LAUNCH_ORDER}
 
 
-SCHEDULES = ("sequential", "concurrent", "grouped", "overlap")
+SCHEDULES = ("sequential", "concurrent", "grouped")
 
 
 class ColumnShard:
     """All populations of cells [cell_lo, cell_hi) resident on one GPU.
 
     Per timestep every population runs once and folds its currents into the
-    shared node rhs/d in LAUNCH_ORDER (synapses, Ih, then the soma
-    populations; Ca_HVA before CaDynamics_E2, which reads its ica).  The
+    shared node rhs/d in LAUNCH_ORDER (Ih, the soma populations -- Ca_HVA
+    before CaDynamics_E2, which reads its ica -- then the synapses).  The
     `schedule` only changes how the launches are arranged -- every schedule
     performs the same operations on every node in the same order, so all
     give bit-identical results (tests/test_gpu_column.py):
@@ -126,13 +126,9 @@ class ColumnShard:
       kernel folds them into the soma nodes in order;
     * "grouped": the soma populations as ONE launch (runner.PopulationGroup,
       chains NaTs2_t | K_Pst | Ca_HVA -> CaDynamics_E2 | SKv3_1) on a side
-      stream, then the combine;
-    * "overlap": Ih joins the group, so the whole per-instance work except
-      the synapses is one launch that runs CONCURRENTLY with the synapse
-      kernel (the synapses fold first, into the nodes they touch); one
-      node-ordered combine (nmodl_combine_nodes) then folds Ih and the soma
-      populations.  3 launches per timestep -- what matters when a rank
-      holds few cells (strong scaling)."""
+      stream beside Ih, then the combine and the synapses: 4 launches per
+      timestep instead of 8 -- what matters when a rank holds few cells
+      (strong scaling)."""
 
     def __init__(self, spec: ColumnSpec, cell_lo: int, cell_hi: int, options_for=None,
                  concurrent_soma: bool = False, reset: bool = True, host: dict | None = None,
@@ -183,10 +179,8 @@ class ColumnShard:
         unique = all(self.devs[m].nodes.seg_unique == 1 for m in SOMA_MECHS)
         if schedule != "sequential" and not unique:
             schedule = "sequential"
-        if schedule == "overlap" and not (reset and self.devs["Ih"].nodes.seg_unique == 1):
-            schedule = "grouped"
         self.schedule = schedule
-        self.grouped = schedule in ("grouped", "overlap")
+        self.grouped = schedule == "grouped"
         self.concurrent = schedule != "sequential"
         self._soma_order = [m for m in LAUNCH_ORDER if m in SOMA_MECHS]
         import ctypes as C
@@ -210,48 +204,16 @@ class ColumnShard:
 
             chains = [[member(m)] for m in self._soma_order if m not in ("Ca_HVA", "cadyn")]
             chains.insert(self._soma_order.index("Ca_HVA"), [member("Ca_HVA"), member("cadyn")])
-            name = "soma"
-            if schedule == "overlap":
-                self.devs["Ih"].nodes.seg_unique = 2
-                chains.insert(0, [member("Ih")])
-                name = "cell"
-            self.group = PopulationGroup(name, chains)
+            self.group = PopulationGroup("soma", chains)
             self._group_stream = rt.Stream()
             self._group_done = rt.Event()
-        if schedule == "overlap":
-            self._overlap_setup()
-
-    def _overlap_setup(self) -> None:
-        """Node maps of the node-ordered combine: which nodes the synapses
-        touched (their fold starts from the synapse sum, the others from 0),
-        the Ih instance of every node and the soma instance of the soma nodes
-        (positions in the node-sorted device stores)."""
-        from . import runtime as rt
-
-        nn = self.nodes.n_nodes
-        syn = self.node_index["ProbAMPANMDA_EMS"]
-        touched = (np.bincount(syn, minlength=nn) > 0).astype(np.uint8)
-
-        def inverse(idx):
-            srt = np.asarray(idx)[np.argsort(idx, kind="stable")]
-            out = np.full(nn, -1, dtype=np.int32)
-            out[srt] = np.arange(len(srt), dtype=np.int32)
-            return out
-
-        maps = [touched, inverse(self.node_index["Ih"]), inverse(self.node_index[self._soma_order[0]])]
-        self._maps = [rt.DeviceBuffer(max(m.nbytes, 8)) for m in maps]
-        for buf, m in zip(self._maps, maps):
-            rt.h2d(buf.ptr, m.ctypes.data, m.nbytes, self.stream)
-        self.stream.sync()
-        syn_nb = self.devs["ProbAMPANMDA_EMS"].nodes
-        syn_nb.assign = 1  # first fold of the step, into the nodes it touches
 
     @property
     def group_members(self) -> list[str]:
         """Populations stepped inside the population-group launch."""
         if not self.grouped:
             return []
-        return [m for m in LAUNCH_ORDER if m in SOMA_MECHS or (m == "Ih" and self.schedule == "overlap")]
+        return [m for m in LAUNCH_ORDER if m in SOMA_MECHS]
 
     @property
     def n_instances(self) -> int:
@@ -292,22 +254,6 @@ class ColumnShard:
                 for stem in LAUNCH_ORDER:
                     self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
                 continue
-            if self.schedule == "overlap":
-                side = self._group_stream
-                self._fork.record(main)
-                rt.stream_wait(side, self._fork)
-                self.group.launch(side, 1)
-                self._group_done.record(side)
-                syn = "ProbAMPANMDA_EMS"
-                self.runners[syn].launch(self.devs[syn], "step_nodes", 1)
-                rt.stream_wait(main, self._group_done)
-                ih, soma = self.devs["Ih"], self.devs[self._soma_order[0]]
-                rt.check(L.nmodl_combine_nodes(
-                    C.c_void_p(self.nodes.node_rhs), C.c_void_p(self.nodes.node_d), self.nodes.n_nodes,
-                    C.c_void_p(self._maps[0].ptr), C.c_void_p(self._maps[1].ptr), C.c_void_p(ih.ptr["i_acc"]),
-                    C.c_void_p(ih.ptr["g_acc"]), C.c_void_p(self._maps[2].ptr), self._iptr, self._gptr,
-                    len(self._soma_order), C.c_void_p(main.handle)), "combine_nodes")
-                continue
             self._reset_nodes()
             self._fork.record(main)
             if self.schedule == "grouped":
@@ -343,7 +289,7 @@ class ColumnShard:
     def kernels_per_step(self) -> int:
         """Our kernels per timestep (memsets not counted)."""
         return {"sequential": len(LAUNCH_ORDER), "concurrent": len(LAUNCH_ORDER) + 1,
-                "grouped": len(LAUNCH_ORDER) - len(SOMA_MECHS) + 2, "overlap": 3}[self.schedule]
+                "grouped": len(LAUNCH_ORDER) - len(SOMA_MECHS) + 2}[self.schedule]
 
     def check(self) -> None:
         for stem in LAUNCH_ORDER:

@@ -653,61 +653,6 @@ NMODL_API int nmodl_combine_unique(double* rhs, double* d, const int* node_index
 }
 
 
-// Node-ordered fold of two groups of one-instance-per-node populations after
-// an earlier kernel folded into (some of) the nodes: thread per node j,
-//   r = base_valid[j] ? rhs[j] : 0       (the earlier fold touched it / not)
-//   r -= i_first[first_of_node[j]]       (a population on every node: Ih)
-//   r -= i_p[second_of_node[j]], p = 0.. (the soma populations, in order)
-// -- the operations the sequential kernels perform, in the same order, with
-// each node handled by one thread (no ordering between threads needed).
-struct nmodl_combine2_args {
-  const double* i[8];
-  const double* g[8];
-  int n_pops;
-};
-__global__ void k_combine_nodes(double* __restrict__ rhs, double* __restrict__ d, long long n_nodes,
-                                const unsigned char* __restrict__ base_valid, const int* __restrict__ first_of_node,
-                                const double* __restrict__ i_first, const double* __restrict__ g_first,
-                                const int* __restrict__ second_of_node, const nmodl_combine2_args a) {
-  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n_nodes;
-       j += (long long)gridDim.x * blockDim.x) {
-    const bool keep = base_valid == nullptr || base_valid[j];
-    double r = keep ? rhs[j] : 0.0, dd = keep ? d[j] : 0.0;
-    const int f = first_of_node ? first_of_node[j] : -1;
-    if (f >= 0) {
-      r = r - i_first[f];
-      dd = dd + g_first[f];
-    }
-    const int c = second_of_node ? second_of_node[j] : -1;
-    if (c >= 0) {
-      for (int p = 0; p < a.n_pops; ++p) {
-        r = r - a.i[p][c];
-        dd = dd + a.g[p][c];
-      }
-    }
-    rhs[j] = r;
-    d[j] = dd;
-  }
-}
-NMODL_API int nmodl_combine_nodes(double* rhs, double* d, long long n_nodes, const unsigned char* base_valid,
-                                  const int* first_of_node, const double* i_first, const double* g_first,
-                                  const int* second_of_node, const double* const* i_ptrs,
-                                  const double* const* g_ptrs, int n_pops, cudaStream_t s) {
-  if (n_pops < 0 || n_pops > 8) return (int)cudaErrorInvalidValue;
-  if (n_nodes <= 0) return 0;
-  nmodl_combine2_args a{};
-  for (int p = 0; p < n_pops; ++p) {
-    a.i[p] = i_ptrs[p];
-    a.g[p] = g_ptrs[p];
-  }
-  a.n_pops = n_pops;
-  long long blocks = (n_nodes + 255) / 256;
-  k_combine_nodes<<<(int)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, s>>>(rhs, d, n_nodes, base_valid,
-                                                                               first_of_node, i_first, g_first,
-                                                                               second_of_node, a);
-  CK(cudaGetLastError());
-  return 0;
-}
 
 // ---------------------------------------------------------------------------
 // NCCL (validation collectives only: the hot path has no exchange).  The

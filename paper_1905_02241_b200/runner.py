@@ -195,11 +195,10 @@ class DeviceInstanceData:
         # never permuted, never downloaded
         self.unset: set[str] = set()
 
-    def reorder(self, perm_ptr: int, stream, arena: "rt.DeviceBuffer | None" = None, sync: bool = True) -> None:
-        """new[k] = old[perm[k]] for every array, into a fresh arena (or the
-        preallocated `arena`; `sync=False` leaves the permutes enqueued)."""
+    def reorder(self, perm_ptr: int, stream) -> None:
+        """new[k] = old[perm[k]] for every array, into a fresh arena."""
         names = list(self.names) + ["i_acc", "g_acc"]
-        arena = arena or rt.DeviceBuffer(self.stride * len(names))
+        arena = rt.DeviceBuffer(self.stride * len(names))
         L = rt.lib()
         new_ptr = {}
         for i, name in enumerate(names):
@@ -208,9 +207,7 @@ class DeviceInstanceData:
                 rt.check(L.nmodl_permute(C.c_void_p(self.ptr[name]), C.c_void_p(dst), C.c_void_p(perm_ptr), self.n,
                                          0, C.c_void_p(stream.handle)), "permute")
             new_ptr[name] = dst
-        if sync:
-            stream.sync()
-        self.arena_prev = None if sync else self.arena  # keep the source alive until the permutes ran
+        stream.sync()
         self.arena = arena  # the old arena returns to the allocator cache
         self.ptr = new_ptr
 
@@ -833,125 +830,9 @@ def simulate(layout, data, steps: int, jac_mode: str = "exact", on_step=None, ru
     return data
 
 
-class _NotChunkable(Exception):
-    """The pipelined path declines (inputs or mechanism outside its scope, or a
-    reported error): the caller runs the one-store path, which reproduces the
-    reference's error semantics exactly.  The host data is still untouched."""
-
-
-def _simulate_nodes_chunked(runner: "CudaRunner", data, steps: int, node_index, node_v, chunks: int, t: dict):
-    """simulate_nodes with the store split into `chunks` contiguous instance
-    ranges, pipelined: every device buffer is allocated and every chunk's
-    node layout sorted first (one host sync), then all H2D copies are
-    enqueued on a second stream, and each chunk is reordered, initialised
-    and stepped on the runner's stream as soon as its copy has landed -- the
-    PCIe upload of the later chunks overlaps the stepping of the earlier
-    ones, with no host sync (no cudaMalloc) until the end.
-
-    Same results, bit for bit, as the one-store path: instances are
-    independent and their voltage is the (constant) node voltage, so a chunk
-    can run all its steps before the next one starts; the node rhs/d of the
-    last step are the in-order folds over all instances, and chunk k's
-    instances follow chunk k-1's in instance order, so chunk 0 assigns the
-    touched nodes (0 - sum) and every later chunk accumulates onto them --
-    the same sequence of roundings as one fold.  The earlier steps fold into
-    scratch node arrays (their rhs/d are overwritten by the next step in the
-    one-store path too).  Any reported error (or a non-finite input) makes it
-    decline before anything was written back (_NotChunkable)."""
-    import time
-
-    clock = time.perf_counter
-    n = int(data.n)
-    if runner.n_newton or runner.abi.rw_scalars or steps < 1 or not np.isfinite(node_v).all():
-        raise _NotChunkable()
-    for a in list(data.arrays.values()) + list(data.acc.values()):
-        if not (a.flags.c_contiguous and a.dtype == np.float64):
-            raise _NotChunkable()
-    t0 = clock()
-    names = list(data.arrays)
-    up = runner.aux_stream()
-    s = runner.stream
-    L = rt.lib()
-    shared = NodeArrays(node_v, stream=s)
-    scratch = [rt.DeviceBuffer(8 * shared.n_nodes) for _ in range(2)]
-    bounds = [n * k // chunks for k in range(chunks + 1)]
-    parts = []
-    for k in range(chunks):  # every allocation and every node sort, up front
-        lo, hi = bounds[k], bounds[k + 1]
-        view = HostInstanceData(hi - lo, {m: a[lo:hi] for m, a in data.arrays.items()},
-                                {m: a[lo:hi] for m, a in data.acc.items()}, data.scalars)
-        dev = DeviceInstanceData(runner, hi - lo, names, data.scalars)
-        dev.unset |= {"v", "i_acc", "g_acc"}
-        nb = runner.prepare_nodes(hi - lo, node_index[lo:hi], shared=shared, stream=s)
-        runner._enqueue_counts(nb)
-        parts.append({"dev": dev, "view": view, "nb": nb, "lo": lo, "hi": hi,
-                      "arena": rt.DeviceBuffer(dev.stride * (len(names) + 2)),
-                      "scan": rt.DeviceBuffer(8 * len(names)), "landed": rt.Event()})
-    s.sync()
-    for p in parts:
-        runner._apply_counts(p["nb"])
-    t["layout"] = clock() - t0
-    t0 = clock()
-    ev0 = rt.Event()
-    ev0.record(up)
-    for p in parts:  # the uploads, all enqueued now on the second stream
-        dev, view = p["dev"], p["view"]
-        for m in names:
-            if m != "v":
-                rt.h2d(dev.ptr[m], view.arrays[m].ctypes.data, view.arrays[m].nbytes, up)
-        p["landed"].record(up)
-    for k, p in enumerate(parts):
-        dev, nb = p["dev"], p["nb"]
-        rt.stream_wait(s, p["landed"])
-        p["c0"], p["c1"] = rt.Event(), rt.Event()
-        p["c0"].record(s)
-        rt.memset(p["scan"].ptr, 0xFF, p["scan"].nbytes, s)
-        for i, m in enumerate(names):
-            if m != "v":
-                rt.check(L.nmodl_first_nonfinite(C.c_void_p(dev.ptr[m]), dev.n, C.c_void_p(p["scan"].ptr + 8 * i),
-                                                 C.c_void_p(s.handle)), "first_nonfinite")
-        dev.reorder(nb.perm, s, arena=p["arena"], sync=False)
-        dev.nodes = nb
-        runner.gather_voltage(dev)
-        runner.launch(dev, "initialize", 1)
-        nb.node_rhs, nb.node_d, nb.assign = scratch[0].ptr, scratch[1].ptr, 1
-        if steps > 1:
-            runner.launch(dev, "step_nodes", steps - 1)
-        nb.node_rhs, nb.node_d, nb.assign = shared.node_rhs, shared.node_d, (1 if k == 0 else 0)
-        runner.launch(dev, "step_nodes", 1)
-        p["c1"].record(s)
-    s.sync()
-    t["steps"] = clock() - t0
-    # device timeline (ms from the first upload): upload landed, chunk start / end
-    t["timeline_ms"] = [(round(ev0.elapsed_ms(p["landed"]), 3), round(ev0.elapsed_ms(p["c0"]), 3),
-                         round(ev0.elapsed_ms(p["c1"]), 3)) for p in parts]
-    for p in parts:
-        p["dev"].arena_prev = None
-        scan = np.empty(len(names), dtype=np.uint64)
-        rt.d2h(scan.ctypes.data, p["scan"].ptr, scan.nbytes, s)
-        s.sync()
-        if any(v != np.uint64(rt.NO_ERROR) for m, v in zip(names, scan) if m != "v"):
-            raise _NotChunkable()
-    st = runner._read_status()
-    if st.err_key != rt.NO_ERROR:
-        runner._reset_status()
-        raise _NotChunkable()
-    t0 = clock()
-    for p in parts:
-        runner.to_host(p["dev"], p["view"], only_dirty=True)
-    out = {}
-    for name in ("node_rhs", "node_d"):
-        arr = np.empty(shared.n_nodes)
-        rt.d2h(arr.ctypes.data, getattr(shared, name), arr.nbytes, s)
-        out[name] = arr
-    s.sync()
-    t["download"] = clock() - t0
-    return data, out["node_rhs"], out["node_d"]
-
-
 def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, node_d=None,
                    jac_mode: str = "exact", runner: CudaRunner | None = None, timings: dict | None = None,
-                   reset: bool = True, chunks: int = 1):
+                   reset: bool = True):
     """node_index run of one mechanism population (builder extension).
 
     Per timestep: v_i = node_v[node_index[i]]; nrn_state; nrn_cur; then
@@ -962,8 +843,6 @@ def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, 
     start from node_rhs/node_d and accumulate across steps instead.
     Instances are initialised with the gathered voltage.  Returns (data,
     node_rhs, node_d); `data` is updated in place in instance order.
-    `chunks` > 1 pipelines the host->device upload with the stepping
-    (_simulate_nodes_chunked; identical results; per-step reset only).
     `timings` (optional dict) receives wall-clock seconds per phase.
     """
     import time
@@ -973,16 +852,6 @@ def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, 
     t0 = clock()
     runner = runner or CudaRunner(layout, jac_mode=jac_mode)
     node_v = np.ascontiguousarray(node_v, dtype=np.float64)
-    if chunks > 1 and reset and node_rhs is None and node_d is None and int(data.n) >= 1024 * chunks:
-        try:
-            out = _simulate_nodes_chunked(runner, data, steps, np.ascontiguousarray(node_index, dtype=np.int32),
-                                          node_v, int(chunks), t)
-            if timings is not None:
-                timings.update(t)
-            return out
-        except _NotChunkable:
-            t = {}
-            t0 = clock()
     # the node layout (node_index upload, stable sort, segments, tiles) is
     # built on a second stream while the instance store uploads
     aux = runner.aux_stream()

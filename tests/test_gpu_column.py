@@ -13,13 +13,13 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("bench_options", [False, True])
-@pytest.mark.parametrize("schedule", ["sequential", "concurrent", "grouped", "overlap"])
+@pytest.mark.parametrize("schedule", ["sequential", "concurrent", "grouped"])
 def test_small_column_matches_oracle(bench_options, schedule):
     """Default builds, and the builds bench.py measures (bench.options_for:
     relaxed rate arithmetic, fast_redo, ... -- here in node_index mode with
     shared nodes and the one-instance-per-node path); every launch schedule
     (one stream, concurrent soma populations, the soma populations as one
-    grouped launch, Ih + soma group overlapping the synapse kernel)."""
+    grouped launch)."""
     from paper_1905_02241_b200.column import COUPLINGS, LAUNCH_ORDER, ColumnShard, ColumnSpec, load_irs, shard_layout
     from paper_1905_02241_b200.instance import init_range
 
@@ -66,10 +66,9 @@ def test_column_shards_add_up():
 
 def test_concurrent_soma_is_bit_identical_and_graph_capturable():
     """Every concurrent schedule (side streams + in-order combine; one
-    grouped soma launch; Ih + soma group overlapping the synapse kernel +
-    node-ordered combine) gives the sequential schedule's node rhs/d and
-    states BIT FOR BIT, also when the step is captured into a CUDA graph (as
-    bench.py does)."""
+    grouped soma launch + combine) gives the sequential schedule's node
+    rhs/d and states BIT FOR BIT, also when the step is captured into a CUDA
+    graph (as bench.py does)."""
     from paper_1905_02241_b200 import runtime as rt
     from paper_1905_02241_b200.column import LAUNCH_ORDER, ColumnShard, ColumnSpec
 
@@ -78,7 +77,7 @@ def test_concurrent_soma_is_bit_identical_and_graph_capturable():
     seq.launch(30)
     seq.check()
     a = seq.nodes.download(seq.stream)
-    for mode in ("concurrent", "grouped", "overlap"):
+    for mode in ("concurrent", "grouped"):
         con = ColumnShard(spec, 0, spec.n_cells, schedule=mode)
         assert con.schedule == mode
         g = rt.capture(con.stream, lambda: con.launch(30))

@@ -220,50 +220,3 @@ def test_node_kernel_cp_async_pipeline_matches_oracle(variant, n, n_nodes, tile)
     assert dev <= TOL, (where, dev)
     _check_nodes(rhs_gpu, d_gpu, rhs_ref, d_ref, terms)
 
-
-@pytest.mark.parametrize("stem,n,n_nodes,steps,chunks", [
-    ("ProbAMPANMDA_EMS", 200_000, 20_000, 60, 4),
-    ("ProbAMPANMDA_EMS", 50_003, 7, 20, 3),        # few huge segments spanning every chunk
-    ("hh_subset", 40_000, 40_000, 30, 5),          # one instance per node
-    ("ProbAMPANMDA_EMS", 10_000, 2_000, 1, 2),     # a single step: no scratch steps
-])
-def test_chunked_pipeline_is_bit_identical(stem, n, n_nodes, steps, chunks):
-    """simulate_nodes(chunks=k): per-chunk upload overlapped with stepping
-    gives the one-store call's states, currents and node rhs/d BIT FOR BIT
-    (chunk 0 assigns the nodes, later chunks accumulate in instance order)."""
-    from bench import options_for
-    from paper_1905_02241_b200.runner import CudaRunner, simulate_nodes
-
-    ir = load_ir(stem)
-    idx, nv = _inputs(n, n_nodes, 5)
-    r = CudaRunner(ir, options=options_for(stem))
-    a, rhs_a, d_a = simulate_nodes(ir, O.init(ir, n, 2), steps, idx, nv, runner=r)
-    t = {}
-    b, rhs_b, d_b = simulate_nodes(ir, O.init(ir, n, 2), steps, idx, nv, runner=r, chunks=chunks, timings=t)
-    assert "layout" in t  # the pipelined path ran (it did not decline)
-    for k in a.arrays:
-        np.testing.assert_array_equal(a.arrays[k].view(np.int64), b.arrays[k].view(np.int64), err_msg=k)
-    for k in a.acc:
-        np.testing.assert_array_equal(a.acc[k].view(np.int64), b.acc[k].view(np.int64), err_msg=k)
-    np.testing.assert_array_equal(rhs_a.view(np.int64), rhs_b.view(np.int64))
-    np.testing.assert_array_equal(d_a.view(np.int64), d_b.view(np.int64))
-
-
-def test_chunked_pipeline_declines_on_error_with_reference_message():
-    """A non-finite input (or a reported error) makes the pipelined path step
-    aside before anything is written back: the one-store path then raises
-    exactly the oracle's error."""
-    from paper_1905_02241_b200.runner import CudaRunner, InterpError, simulate_nodes
-
-    ir = load_ir("ProbAMPANMDA_EMS")
-    n, n_nodes = 20_000, 1000
-    idx, nv = _inputs(n, n_nodes, 9)
-    data = O.init(ir, n, 4)
-    data.arrays["tau_r_AMPA"][12_345] = np.nan
-    ref = O.init(ir, n, 4)
-    ref.arrays["tau_r_AMPA"][12_345] = np.nan
-    with pytest.raises(Exception) as want:
-        N.simulate_nodes(ir, ref, 10, idx, nv)
-    with pytest.raises(InterpError) as got:
-        simulate_nodes(ir, data, 10, idx, nv, runner=CudaRunner(ir), chunks=4)
-    assert str(got.value) == str(want.value)

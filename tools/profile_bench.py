@@ -116,7 +116,7 @@ def parent(out_dir: Path, workloads: list[str]) -> None:
         # the per-step kernel count is known after setup; a dry child run is
         # cheap compared to the capture, so read it from bench's own tables
         if wl == "column":
-            per_step = {"sequential": 7, "concurrent": 8, "grouped": 4, "overlap": 3}[bench._column_mode()["schedule"]]
+            per_step = {"sequential": 7, "concurrent": 8, "grouped": 4}[bench._column_mode()["schedule"]]
             regex = "regex:_k_step|combine"
         else:
             per_step = len(bench.WORKLOADS[wl]["mechs"])

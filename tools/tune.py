@@ -106,7 +106,7 @@ def main():
         for stem in stems_:
             for d in deltas:
                 opts = dataclasses.replace(options_for(stem), **{k: getattr(d, k) for k in keys})
-                nodes = 1_000_000 if stem == "ProbAMPANMDA_EMS" else 0
+                nodes = int(os.environ.get("TUNE_NODES", 1_000_000)) if stem == "ProbAMPANMDA_EMS" else 0
                 try:
                     res = run(stem, opts, nodes)
                 except Exception as exc:  # noqa: BLE001
@@ -130,7 +130,7 @@ def main():
     rt.require_device(0)
     for stem in stems:
         for opts in VARIANTS:
-            nodes = 1_000_000 if stem == "ProbAMPANMDA_EMS" else 0
+            nodes = int(os.environ.get("TUNE_NODES", 1_000_000)) if stem == "ProbAMPANMDA_EMS" else 0
             try:
                 res = run(stem, opts, nodes)
             except Exception as exc:  # noqa: BLE001

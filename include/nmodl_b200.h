@@ -171,6 +171,8 @@ int nmodl_nccl_allgather_f64(void *comm, const double *send, double *recv, long 
  *                          reduced into node rhs/d in instance order
  *   <mech>_abi             JSON description of <mech>_data (field order)
  *   <mech>_abi_size        sizeof(<mech>_data)
+ *   <mech>_step_nodes_ctas resident CTAs of the node kernel on the current
+ *                          device (the host sizes node tiles to whole waves)
  */
 #define NMODL_B200_MECHANISM(mech)                                                    \
   int mech##_initialize(const void *md, int nsteps, nmodl_stream_t s, int flags);     \
@@ -179,7 +181,22 @@ int nmodl_nccl_allgather_f64(void *comm, const double *send, double *recv, long 
   int mech##_step(const void *md, int nsteps, nmodl_stream_t s, int flags);           \
   int mech##_step_nodes(const void *md, int nsteps, nmodl_stream_t s, int flags);     \
   const char *mech##_abi(void);                                                       \
-  long long mech##_abi_size(void);
+  long long mech##_abi_size(void);                                                    \
+  int mech##_step_nodes_ctas(void);
+
+/* ---- population group library (libgroup_<name>-<hash>.so) -------------
+ * Several one-instance-per-node populations stepped by one launch
+ * (codegen_cuda.emit_group; an extension -- the reference steps one
+ * mechanism per call, interp.py:456-471).  `a` points to a host copy of
+ * `<name>_args`: the members' <mech>_data structs back to back, then
+ * `long long cta[n_chains + 1]` (chain c owns CTAs [cta[c], cta[c+1])).
+ *
+ *   <name>_step_unique     `nsteps` group launches on `s` (0 or cudaError_t)
+ *   <name>_args_size       sizeof(<name>_args)
+ */
+#define NMODL_B200_GROUP(name)                                                        \
+  int name##_step_unique(const void *a, int nsteps, nmodl_stream_t s, int flags);     \
+  long long name##_args_size(void);
 
 #ifdef __cplusplus
 }

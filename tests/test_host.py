@@ -146,7 +146,8 @@ def test_mechanism_library_exports_and_abi(stem):
     ir = load_ir(stem)
     mb = build_mechanism(ir)
     lib = ctypes.CDLL(str(mb.so_path))
-    for k in ("initialize", "state_update", "current_update", "step", "step_nodes", "abi", "abi_size"):
+    for k in ("initialize", "state_update", "current_update", "step", "step_nodes", "abi", "abi_size",
+              "step_nodes_ctas"):
         assert hasattr(lib, f"{mb.symbol}_{k}")
     f = getattr(lib, f"{mb.symbol}_abi")
     f.restype = ctypes.c_char_p

@@ -32,6 +32,9 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tools"))
 
 WARM = 3
+# bench.py warms the secondary workloads 100 steps (cdp5ish's Newton iteration
+# counts fall over the first ~100 steps after nrn_init): profile the same state
+WARM_FOR = {"kinetic1m": 100}
 FP64_OPCODES = ("DFMA", "DMUL", "DADD", "DSETP", "DMNMX")  # the FP64 pipe (paper_1905_02241_b200.analysis)
 
 
@@ -77,7 +80,7 @@ def child(workload: str, out: str) -> None:
         s0 = pops[0].runner.stream
         for p in pops:
             p.runner.stream = s0
-        for _ in range(WARM + 1):
+        for _ in range(WARM_FOR.get(workload, WARM) + 1):
             for p in pops:
                 p.launch(1)
         s0.sync()
@@ -123,7 +126,7 @@ def parent(out_dir: Path, workloads: list[str]) -> None:
             regex = "regex:_k_step"
         rep = out_dir / f"{wl}"
         cmd = ["ncu", "--set", "full", "--import-source", "on", "--clock-control", "none", "-k", regex,
-               "--launch-skip", str(WARM * per_step), "--launch-count", str(per_step), "-f", "-o", str(rep),
+               "--launch-skip", str(WARM_FOR.get(wl, WARM) * per_step), "--launch-count", str(per_step), "-f", "-o", str(rep),
                sys.executable, __file__, "--child", wl, str(meta)]
         print(" ".join(cmd), flush=True)
         proc = subprocess.run(cmd, capture_output=True, text=True)
@@ -143,7 +146,7 @@ def parent(out_dir: Path, workloads: list[str]) -> None:
                 "kernel": name, "workload": wl, "instances": k["n"], "dram_bytes": dram,
                 "dram_read": _num(r["dram__bytes_read.sum"]), "dram_write": _num(r["dram__bytes_write.sum"]),
                 "us": _num(r["gpu__time_duration.sum"]) / 1e3, "bytes_per_launch": k.get("bytes_per_launch"),
-                "capture": f"ncu --set full, one launch after {WARM} warm-up steps; summary "
+                "capture": f"ncu --set full, one launch after {WARM_FOR.get(wl, WARM)} warm-up steps; summary "
                            f"profiles/{tag}/{wl}.json",
             }
         subprocess.run([sys.executable, str(ROOT / "tools" / "ncu_summary.py"), str(out_dir),

@@ -447,6 +447,7 @@ def run_workload(name, args, dist, sustained=True):
                 evs[k][j + 1].record_external(s0)
 
     graph = rt.capture(s0, body)
+    graph.upload(s0)
     ev_a, ev_b = rt.Event(), rt.Event()
     dist.barrier()
     s0.sync()
@@ -469,6 +470,7 @@ def run_workload(name, args, dist, sustained=True):
     if sustained and flush is None:
         S = int(min(20000, max(K, SUSTAINED_S / max(total_ms / K / 1e3, 1e-9))))
         g2 = rt.capture(s0, lambda: [p.launch(1) for _ in range(S) for p in pops])
+        g2.upload(s0)
         dist.barrier()
         s0.sync()
         with ClockSampler(phys) as clk2:
@@ -569,6 +571,7 @@ def run_column(args, dist, sustained=True):
     shard.check()
     ev_a, ev_b = rt.Event(), rt.Event()
     graph = rt.capture(s0, lambda: shard.launch(K))
+    graph.upload(s0)
     dist.barrier()
     s0.sync()
     phys = _physical_gpu(dist.device)
@@ -585,6 +588,7 @@ def run_column(args, dist, sustained=True):
     if sustained:
         S = int(min(20000, max(K, SUSTAINED_S / max(ms / K / 1e3, 1e-9))))
         g2 = rt.capture(s0, lambda: shard.launch(S))
+        g2.upload(s0)
         dist.barrier()
         s0.sync()
         with ClockSampler(phys) as clk2:
@@ -605,6 +609,7 @@ def run_column(args, dist, sustained=True):
     reps = 10
     for m in LAUNCH_ORDER:
         g = rt.capture(s0, lambda m=m: shard.runners[m].launch(shard.devs[m], "step_nodes", reps))
+        g.upload(s0)
         a, b = rt.Event(), rt.Event()
         a.record(s0)
         g.launch(s0)
@@ -1001,7 +1006,7 @@ def main():
             del r
     cpu = None
     if dist.rank == 0 and args.gpus == 1 and not args.no_cpu:
-        cpu = reference_arm(args.workload, K=3, W=1, budget_s=20.0)
+        cpu = reference_arm(args.workload, K=20, W=5, budget_s=30.0)
         if cpu is not None and not column:
             cpu["numpy_oracle"] = numpy_oracle_rate(args.workload)
     if dist.rank == 0:

@@ -98,6 +98,8 @@ int nmodl_event_elapsed_ms(nmodl_event_t a, nmodl_event_t b, float *ms);
 /* CUDA-graph capture of the per-timestep launch loop */
 int nmodl_capture_begin(nmodl_stream_t s);
 int nmodl_capture_end(nmodl_stream_t s, nmodl_graph_t *out);
+/* upload the graph to the device before its first (timed) launch */
+int nmodl_graph_upload(nmodl_graph_t g, nmodl_stream_t s);
 int nmodl_graph_launch(nmodl_graph_t g, nmodl_stream_t s);
 int nmodl_graph_destroy(nmodl_graph_t g);
 /* status block */
@@ -137,6 +139,8 @@ int nmodl_selftest_exp(const double *x, double *out_a, double *out_b, long long 
 /* self-test: out[i] = nmodl::div_a(a[i], b[i]) (relaxed division, CudaOptions.div_approx);
  * a signalling-NaN marker where the branch-free form disagrees without flagging */
 int nmodl_selftest_div_approx(const double *a, const double *b, double *out, long long n, nmodl_stream_t s);
+/* shared-reciprocal division div_ry(a, b, RN(1/b)) (LU pivots, CudaOptions.lu_rcp): must equal a / b */
+int nmodl_selftest_div_ry(const double *a, const double *b, double *out, long long n, nmodl_stream_t s);
 /* self-test: out[i] = nmodl::exp16(x[i]) (shared-memory table exp, CudaOptions.exp_smem);
  * flag[i] bit 0 = fast form flagged, bit 1 = fast and safe forms disagree without a flag */
 int nmodl_selftest_exp_smem(const double *x, double *out, unsigned *flag, long long n, nmodl_stream_t s);

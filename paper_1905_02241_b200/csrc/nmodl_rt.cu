@@ -170,6 +170,13 @@ NMODL_API int nmodl_capture_end(cudaStream_t s, cudaGraphExec_t* out) {
   if (e != cudaSuccess) return fail(e, "cudaGraphInstantiate");
   return 0;
 }
+// upload an instantiated graph's work descriptors to the device ahead of its
+// first launch (otherwise the first replay pays for it: ~10 us per step of a
+// 200-step, 800-node column graph)
+NMODL_API int nmodl_graph_upload(cudaGraphExec_t g, cudaStream_t s) {
+  CK(cudaGraphUpload(g, s));
+  return 0;
+}
 NMODL_API int nmodl_graph_launch(cudaGraphExec_t g, cudaStream_t s) {
   CK(cudaGraphLaunch(g, s));
   return 0;
@@ -588,6 +595,25 @@ __global__ void k_selftest_div_approx(const double* __restrict__ a, const double
 }
 NMODL_API int nmodl_selftest_div_approx(const double* a, const double* b, double* out, long long n, cudaStream_t s) {
   k_selftest_div_approx<<<256, 256, 0, s>>>(a, b, out, n);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// shared-reciprocal IEEE division (CudaOptions.lu_rcp): out = div_ry(a, b,
+// RN(1/b)); a fast-form result that differs without a flag is marked with a
+// signalling-NaN payload
+__global__ void k_selftest_div_ry(const double* __restrict__ a, const double* __restrict__ b,
+                                  double* __restrict__ out, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    unsigned f = 0;
+    const double y = nmodl::rcp_rn(b[i]);
+    const double fast = nmodl::div_ryf(a[i], b[i], y, f);
+    const double safe = nmodl::div_ry(a[i], b[i], y);
+    out[i] = (f == 0 && __double_as_longlong(fast) != __double_as_longlong(safe)) ? __longlong_as_double(0x7ff4dead00000000ll) : safe;
+  }
+}
+NMODL_API int nmodl_selftest_div_ry(const double* a, const double* b, double* out, long long n, cudaStream_t s) {
+  k_selftest_div_ry<<<256, 256, 0, s>>>(a, b, out, n);
   CK(cudaGetLastError());
   return 0;
 }

@@ -77,6 +77,7 @@ _SIGS = {
     "nmodl_capture_begin": (C.c_int, [C.c_void_p]),
     "nmodl_capture_end": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "nmodl_graph_launch": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "nmodl_graph_upload": (C.c_int, [C.c_void_p, C.c_void_p]),
     "nmodl_graph_destroy": (C.c_int, [C.c_void_p]),
     "nmodl_status_reset": (C.c_int, [C.c_void_p, C.c_void_p]),
     "nmodl_status_size": (C.c_int, []),
@@ -97,6 +98,7 @@ _SIGS = {
     "nmodl_gather_v": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
     "nmodl_selftest_exp": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
     "nmodl_selftest_div_approx": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
+    "nmodl_selftest_div_ry": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
     "nmodl_selftest_exp_smem": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
 }
 RUNTIME_SYMBOLS = tuple(_SIGS)
@@ -305,6 +307,12 @@ class Graph:
 
     def launch(self, stream: Stream) -> None:
         check(lib().nmodl_graph_launch(C.c_void_p(self.handle), C.c_void_p(stream.handle)), "graph_launch")
+
+    def upload(self, stream: Stream) -> None:
+        """Move the work descriptors to the device now (and wait), so the
+        first launch -- a timed one -- does not pay for it."""
+        check(lib().nmodl_graph_upload(C.c_void_p(self.handle), C.c_void_p(stream.handle)), "graph_upload")
+        stream.sync()
 
     def __del__(self):
         try:

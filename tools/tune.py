@@ -62,6 +62,7 @@ def run(stem, opts, nodes=0, steps=30):
             b.record_external(r.stream)
 
     g = rt.capture(r.stream, body)
+    g.upload(r.stream)
     g.launch(r.stream)
     r.stream.sync()
     total = sum(a.elapsed_ms(b) for a, b in evs)

@@ -139,8 +139,6 @@ int nmodl_selftest_exp(const double *x, double *out_a, double *out_b, long long 
 /* self-test: out[i] = nmodl::div_a(a[i], b[i]) (relaxed division, CudaOptions.div_approx);
  * a signalling-NaN marker where the branch-free form disagrees without flagging */
 int nmodl_selftest_div_approx(const double *a, const double *b, double *out, long long n, nmodl_stream_t s);
-/* shared-reciprocal division div_ry(a, b, RN(1/b)) (LU pivots, CudaOptions.lu_rcp): must equal a / b */
-int nmodl_selftest_div_ry(const double *a, const double *b, double *out, long long n, nmodl_stream_t s);
 /* self-test: out[i] = nmodl::exp16(x[i]) (shared-memory table exp, CudaOptions.exp_smem);
  * flag[i] bit 0 = fast form flagged, bit 1 = fast and safe forms disagree without a flag */
 int nmodl_selftest_exp_smem(const double *x, double *out, unsigned *flag, long long n, nmodl_stream_t s);

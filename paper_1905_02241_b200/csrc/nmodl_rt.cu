@@ -599,25 +599,6 @@ NMODL_API int nmodl_selftest_div_approx(const double* a, const double* b, double
   return 0;
 }
 
-// shared-reciprocal IEEE division (CudaOptions.lu_rcp): out = div_ry(a, b,
-// RN(1/b)); a fast-form result that differs without a flag is marked with a
-// signalling-NaN payload
-__global__ void k_selftest_div_ry(const double* __restrict__ a, const double* __restrict__ b,
-                                  double* __restrict__ out, long long n) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    unsigned f = 0;
-    const double y = nmodl::rcp_rn(b[i]);
-    const double fast = nmodl::div_ryf(a[i], b[i], y, f);
-    const double safe = nmodl::div_ry(a[i], b[i], y);
-    out[i] = (f == 0 && __double_as_longlong(fast) != __double_as_longlong(safe)) ? __longlong_as_double(0x7ff4dead00000000ll) : safe;
-  }
-}
-NMODL_API int nmodl_selftest_div_ry(const double* a, const double* b, double* out, long long n, cudaStream_t s) {
-  k_selftest_div_ry<<<256, 256, 0, s>>>(a, b, out, n);
-  CK(cudaGetLastError());
-  return 0;
-}
-
 // shared-memory table exp (CudaOptions.exp_smem): out = exp16(x); flag bit 0 =
 // fast form flagged, bit 1 = fast and safe forms disagree without a flag
 __global__ void k_selftest_exp_smem(const double* __restrict__ x, double* __restrict__ a,

@@ -55,8 +55,6 @@ def variants():
     for st in ("na6", "cdp5ish", "corpus_fourstate", "corpus_pump", "corpus_fourstate.nopass", "corpus_pump.nopass"):
         out.append((st, dict(lu_spec=True)))
         out.append((st, dict(lu_spec=True, fast_path=True, fast_redo=True, pipe=True)))
-        out.append((st, dict(lu_rcp=True)))
-        out.append((st, dict(lu_spec=True, lu_rcp=True, fast_path=True, fast_redo=True, pipe=True)))
     for st in ("hh_subset", "ProbAMPANMDA_EMS", "corpus_exp2syn"):
         out.append((st, dict(fmad=True)))
     for st, kw in FALLBACK_BENCH:

@@ -241,8 +241,14 @@ def init_group(device_count: int | None = None):
         device_count = rt.device_count()
     ndev = max(device_count, 1)
     device = local % ndev
-    if ndev >= world:
-        return NcclGroup(rank, world, device, bootstrap_dir()), device
+    if ndev >= world and os.environ.get("NMODL_GROUP", "nccl") == "nccl":
+        try:
+            return NcclGroup(rank, world, device, bootstrap_dir()), device
+        except Exception as exc:  # noqa: BLE001 -- validation collectives only: keep going
+            import sys
+
+            print(f"[parallel] rank {rank}: NCCL group unavailable ({exc}); using the file group", file=sys.stderr)
+            return FileGroup(bootstrap_dir() / "file_fallback", rank, world), device
     return FileGroup(bootstrap_dir() / "file", rank, world), device
 
 

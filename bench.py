@@ -100,8 +100,9 @@ def options_for(stem: str):
         "K_Pst": CudaOptions(ilp=2, min_blocks=2, pipe=True, recip=True, quot=True, div_approx=True, exp_smem=True,
                              exp_share=True, fast_redo=True),  # 0.0717 -> 0.0574 ms
         "Ca_HVA": CudaOptions(ilp=2, min_blocks=2, pipe=True, recip=True, div_approx=True, fast_redo=True),  # 0.0707 -> 0.0561
-        "SKv3_1": CudaOptions(ilp=1, pipe=True, grid_waves=4, div_approx=True, fast_redo=True),  # 0.0500 -> 0.0426 ms
+        "SKv3_1": CudaOptions(ilp=2, grid_waves=4, div_approx=True, fast_redo=True),  # 0.0500 -> 0.0426 -> 0.0388 ms (r02 ilp=2)
         "Ih": CudaOptions(ilp=2, pipe=True, grid_waves=4, recip=True, div_approx=True, fast_redo=True),  # 0.0474 -> 0.0392 ms
+        "cadyn": CudaOptions(pipe=True, min_blocks=2),  # 0.0471 -> 0.0462 ms (profiles/r02/tune_small.jsonl)
         "na6": CudaOptions(ilp=1, min_blocks=2, pipe=True, fast_redo=True, lu_spec=True),  # 0.0485 -> 0.0369 ms
         "cdp5ish": CudaOptions(ilp=1, min_blocks=2, pipe=True, div_approx=True, fast_redo=True, lu_spec=True),  # 0.0583 -> 0.0390
     }

@@ -359,7 +359,8 @@ class Population:
 
     @property
     def kernel_name(self):
-        return f"{self.runner.mb.symbol}_k_{self.kernel}"
+        k = self.runner.node_kernel(self.dev) if (self.kernel == "step_nodes" and self.dev is not None) else self.kernel
+        return f"{self.runner.mb.symbol}_k_{k}"
 
     def setup_device(self):
         r = self.runner

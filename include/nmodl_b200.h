@@ -173,6 +173,8 @@ int nmodl_nccl_allgather_f64(void *comm, const double *send, double *recv, long 
  *                          reduced into node rhs/d in instance order
  *   <mech>_abi             JSON description of <mech>_data (field order)
  *   <mech>_abi_size        sizeof(<mech>_data)
+ *   <mech>_step_unique     (pipelined builds) step_nodes for one instance per
+ *                          node: cp.async pipeline, no segment reduction
  *   <mech>_step_nodes_ctas resident CTAs of the node kernel on the current
  *                          device (the host sizes node tiles to whole waves)
  */

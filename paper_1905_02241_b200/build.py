@@ -126,7 +126,35 @@ def build_mechanism(layout, options: CudaOptions | None = None, fmad: bool | Non
             tmp = so.with_suffix(f".so.tmp{os.getpid()}.{threading.get_ident()}")
             _run([nvcc_path(), *flags, str(cu), "-o", str(tmp)], out_dir / f"{stem}.log")
             tmp.replace(so)
+        else:
+            _touch(so)
     return MechBuild(so, cu, abi, printer.mech, text)
+
+
+def _touch(path: Path) -> None:
+    """Mark a cached library as in use (prune_stale keeps what a build touched)."""
+    try:
+        os.utime(path)
+    except OSError:
+        pass
+
+
+def prune_stale(since: float) -> int:
+    """Remove the generated sources / logs / libraries in _build/mech that no
+    build since `since` (a time.time() stamp) produced or reused -- the
+    content-addressed cache otherwise keeps every variant ever built, and the
+    tree travels to the GPU box.  Returns the number of files removed."""
+    out_dir = BUILD / "mech"
+    if not out_dir.is_dir():
+        return 0
+    keep = {p.name[3:-3] for p in out_dir.glob("lib*.so") if p.stat().st_mtime >= since - 1.0}
+    removed = 0
+    for p in out_dir.iterdir():
+        stem = p.name[3:-3] if p.name.startswith("lib") and p.name.endswith(".so") else p.name.rsplit(".", 1)[0]
+        if stem not in keep:
+            p.unlink()
+            removed += 1
+    return removed
 
 
 def build_many(layouts, options: CudaOptions | None = None, fmad: bool | None = None,
@@ -169,4 +197,6 @@ def build_group(name: str, chains, fmad: bool = False, force: bool = False) -> G
             tmp = so.with_suffix(f".so.tmp{os.getpid()}.{threading.get_ident()}")
             _run([nvcc_path(), *flags, str(cu), "-o", str(tmp)], out_dir / f"{stem}.log")
             tmp.replace(so)
+        else:
+            _touch(so)
     return GroupBuild(so, cu, _cname(name), abis, unit.text)

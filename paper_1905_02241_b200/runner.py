@@ -271,8 +271,10 @@ class CudaRunner:
         self.lib = C.CDLL(str(self.mb.so_path))
         sym = self.mb.symbol
         self.entry = {}
-        for k in KERNELS:
-            fn = getattr(self.lib, f"{sym}_{k}")
+        for k in KERNELS + ("step_unique",):
+            fn = getattr(self.lib, f"{sym}_{k}", None)
+            if fn is None and k == "step_unique":
+                continue  # emitted for pipelined builds only
             fn.restype = C.c_int
             fn.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int]
             self.entry[k] = fn
@@ -422,6 +424,15 @@ class CudaRunner:
                 dev.scalars[s] = float(v)
 
     # ---- execution -----------------------------------------------------------------
+    def node_kernel(self, dev: DeviceInstanceData) -> str:
+        """The kernel a `step_nodes` launch of `dev` runs: `step_unique` (the
+        direct kernels' cp.async pipeline, one instance per node) when the
+        build has it and every occupied node holds one instance, else the
+        tiled `step_nodes` with its in-order segment reduction."""
+        if dev.nodes is not None and dev.nodes.seg_unique in (1, 2) and "step_unique" in self.entry:
+            return "step_unique"
+        return "step_nodes"
+
     def launch(self, dev: DeviceInstanceData, kernel_name: str, steps: int = 1, newton_rec: int = 0) -> None:
         """Enqueue `steps` launches on the runner's stream (no sync, no checks)."""
         if kernel_name == "step_nodes" and dev.nodes is None:
@@ -429,7 +440,8 @@ class CudaRunner:
         md = self._struct(dev, newton_rec)
         dev.dirty |= self._writes[kernel_name]
         rt.set_device(self.device)
-        rc = self.entry[kernel_name](C.byref(md), int(steps), C.c_void_p(self.stream.handle), self.flags)
+        entry = self.entry[self.node_kernel(dev) if kernel_name == "step_nodes" else kernel_name]
+        rc = entry(C.byref(md), int(steps), C.c_void_p(self.stream.handle), self.flags)
         rt.check(rc, f"launch {self.mb.symbol}_{kernel_name}")
 
     def run_kernel(self, data, kernel_name: str, steps: int = 1):

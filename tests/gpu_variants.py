@@ -57,6 +57,8 @@ def variants():
         out.append((st, dict(lu_spec=True, fast_path=True, fast_redo=True, pipe=True)))
     for st in ("hh_subset", "ProbAMPANMDA_EMS", "corpus_exp2syn"):
         out.append((st, dict(fmad=True)))
+    for ilp in (1, 2):
+        out.append(("corpus_exp2syn", dict(fast_path=True, fast_redo=True, pipe=True, ilp=ilp)))
     for st, kw in FALLBACK_BENCH:
         out.append((st, kw))
     for st in RELAXED_STEMS:

@@ -220,3 +220,37 @@ def test_node_kernel_cp_async_pipeline_matches_oracle(variant, n, n_nodes, tile)
     assert dev <= TOL, (where, dev)
     _check_nodes(rhs_gpu, d_gpu, rhs_ref, d_ref, terms)
 
+
+
+@pytest.mark.parametrize("stem", ["Ih", "hh_subset", "NaTs2_t", "cadyn", "K_Pst"])
+@pytest.mark.parametrize("sparse", [False, True])
+def test_step_unique_kernel(stem, sparse):
+    """One instance per node with a pipelined build (bench.options_for): the
+    `step_unique` kernel (direct kernels' cp.async pipeline and ILP, v
+    gathered from the node, each instance folding into its own node) gives
+    the tiled step_nodes path's states, currents and node rhs/d BIT FOR BIT,
+    and matches the oracle.  `sparse`: fewer instances than nodes (somas)."""
+    from bench import options_for
+    from paper_1905_02241_b200.runner import CudaRunner, simulate_nodes
+
+    ir = load_ir(stem)
+    n, n_nodes = 9001, (3 * 9001 if sparse else 9001)
+    idx = np.random.default_rng(5).permutation(n_nodes)[:n].astype(np.int32)
+    nv = np.random.default_rng(6).uniform(-80, 40, n_nodes)
+    terms = {}
+    ref, rhs_ref, d_ref = N.simulate_nodes(ir, O.init(ir, n, 2), 60, idx, nv, terms=terms)
+    fast = CudaRunner(ir, options=options_for(stem))
+    assert "step_unique" in fast.entry
+    a, rhs_a, d_a = simulate_nodes(ir, O.init(ir, n, 2), 60, idx, nv, runner=fast)
+    tiled = CudaRunner(ir, options=options_for(stem))
+    del tiled.entry["step_unique"]  # force the tiled node kernel
+    b, rhs_b, d_b = simulate_nodes(ir, O.init(ir, n, 2), 60, idx, nv, runner=tiled)
+    for k in a.arrays:
+        np.testing.assert_array_equal(a.arrays[k].view(np.int64), b.arrays[k].view(np.int64), err_msg=k)
+    for k in a.acc:
+        np.testing.assert_array_equal(a.acc[k].view(np.int64), b.acc[k].view(np.int64), err_msg=k)
+    np.testing.assert_array_equal(rhs_a.view(np.int64), rhs_b.view(np.int64))
+    np.testing.assert_array_equal(d_a.view(np.int64), d_b.view(np.int64))
+    dev, where = parity(ir, ref, a)
+    assert dev <= TOL, (where, dev)
+    _check_nodes(rhs_a, d_a, rhs_ref, d_ref, terms)

@@ -63,7 +63,7 @@ def child(workload: str, out: str) -> None:
             if m in shard.group_members:
                 continue
             r, d = shard.runners[m], shard.devs[m]
-            rows.append({"kernel": f"{r.mb.symbol}_k_step_nodes", "build": r.mb.so_path.stem[3:], "n": d.n})
+            rows.append({"kernel": f"{r.mb.symbol}_k_{r.node_kernel(d)}", "build": r.mb.so_path.stem[3:], "n": d.n})
         if shard.grouped:
             gb = shard.group.gb
             rows.append({"kernel": f"{gb.symbol}_k_step_unique", "build": gb.so_path.stem[3:],

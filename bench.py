@@ -106,7 +106,12 @@ def options_for(stem: str):
         "na6": CudaOptions(ilp=1, min_blocks=2, pipe=True, fast_redo=True, lu_spec=True),  # 0.0485 -> 0.0369 ms
         "cdp5ish": CudaOptions(ilp=1, min_blocks=2, pipe=True, div_approx=True, fast_redo=True, lu_spec=True),  # 0.0583 -> 0.0390
     }
-    return tuned.get(stem, CudaOptions())
+    import dataclasses
+
+    # programmatic dependent launch for every kernel: the next step's CTAs are
+    # scheduled while the previous grid drains (column 357 -> 352 us, 12.5k
+    # cells 56.3 -> 54.3 us; profiles/r02/pdl_*.json); NMODL_PDL=0 turns it off
+    return dataclasses.replace(tuned.get(stem, CudaOptions()), pdl=os.environ.get("NMODL_PDL", "1") == "1")
 
 
 RELAXED_NOTE = ("fp64 throughout; rate code uses reciprocal/quotient shadows (X/(1/E) -> X*E), <=2-ulp division, "

@@ -439,19 +439,27 @@ def run_workload(name, args, dist, sustained=True):
     s0.sync()
     for p in pops:
         p.runner.check(p.dev)
-    # the timed graph: K steps, an external event record before the step and
-    # after every population's launch (kernel durations inside this replay)
+    # the timed graph: K steps.  External event records before a step and
+    # after every population's launch time each kernel inside this replay:
+    # every step when an L2 flush runs between steps (the flush is excluded
+    # from the step time), else the first min(K, 20) steps of a multi-
+    # population step (an event node between two kernels also cuts their
+    # programmatic-dependent-launch edge, so the other steps run without
+    # them); a single-population step needs none (its kernel IS the step).
     P = len(pops)
-    evs = [[rt.Event() for _ in range(P + 1)] for _ in range(K)]
+    E = K if flush is not None else (0 if P == 1 else min(K, 20))
+    evs = [[rt.Event() for _ in range(P + 1)] for _ in range(E)]
 
     def body():
         for k in range(K):
             if flush is not None:
                 flush(s0)
-            evs[k][0].record_external(s0)
+            if k < E:
+                evs[k][0].record_external(s0)
             for j, p in enumerate(pops):
                 p.launch(1)
-                evs[k][j + 1].record_external(s0)
+                if k < E:
+                    evs[k][j + 1].record_external(s0)
 
     graph = rt.capture(s0, body)
     graph.upload(s0)
@@ -465,10 +473,12 @@ def run_workload(name, args, dist, sustained=True):
         ev_b.record(s0)
         ev_b.sync()
     graph_ms = ev_a.elapsed_ms(ev_b)
-    per_pop_ms = [sum(evs[k][j].elapsed_ms(evs[k][j + 1]) for k in range(K)) for j in range(P)]
-    steps_ms = sum(evs[k][0].elapsed_ms(evs[k][P]) for k in range(K))
     # with a flush the timed region is the steps only (flush kernels excluded)
-    total_ms = steps_ms if flush is not None else graph_ms
+    total_ms = sum(evs[k][0].elapsed_ms(evs[k][P]) for k in range(K)) if flush is not None else graph_ms
+    if E:  # per-population launch durations, scaled from the evented steps to K
+        per_pop_ms = [sum(evs[k][j].elapsed_ms(evs[k][j + 1]) for k in range(E)) * K / E for j in range(P)]
+    else:
+        per_pop_ms = [total_ms]
     del graph
     for p in pops:
         p.runner.check(p.dev)
@@ -505,7 +515,7 @@ def run_workload(name, args, dist, sustained=True):
     key = f"{dom.build_key}@{dom.n}"
     roof = _roofline(dom.kernel_name, dom.launch_bytes(), _fp64_instr(dom.ir, dom.n, key), per_pop_ms[j] / K, [key],
                      sm_mhz)
-    roof["share_of_step"] = per_pop_ms[j] / max(sum(per_pop_ms), 1e-30)
+    roof["share_of_step"] = per_pop_ms[j] / max(total_ms, 1e-30)
     roof["model"] = _describe(dom)
     from paper_1905_02241_b200.parallel import device_checksums
 

@@ -631,6 +631,10 @@ struct nmodl_combine_args {
 };
 __global__ void k_combine_unique(double* __restrict__ rhs, double* __restrict__ d, const int* __restrict__ node_index,
                                  long long n, const nmodl_combine_args a) {
+  // a following kernel launched for programmatic dependent launch (the
+  // synapse step, CudaOptions.pdl) may be scheduled now; it waits for this
+  // grid's completion before it reads anything
+  asm volatile("griddepcontrol.launch_dependents;");
   for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
     const int nd = node_index[j];
     double r = rhs[nd], dd = d[nd];

@@ -434,3 +434,28 @@ def test_codegen_hazards_rwglobal():
     first, second = body.index("I.s = I.v;"), body.rindex("NM_EXP")
     exps_of_s = re.findall(r"const double (t_xs\d+) = NM_EXP\(\(double\)\(\(rwglobal_K\[\d+\] \* I\.s\)\)\);", body)
     assert len(exps_of_s) == 2 and first < second
+
+
+def test_prune_stale_keeps_what_a_build_touched(tmp_path, monkeypatch):
+    """build.prune_stale: a cached library reused (touched) since the stamp
+    stays with its source and log; one nobody built or reused goes."""
+    import os
+    import time
+
+    from paper_1905_02241_b200 import build as B
+
+    mech = tmp_path / "mech"
+    mech.mkdir()
+    monkeypatch.setattr(B, "BUILD", tmp_path)
+    old = time.time() - 100
+    for stem in ("hh-aaaa", "hh-bbbb", "group_soma-cccc"):
+        for name in (f"lib{stem}.so", f"{stem}.cu", f"{stem}.log"):
+            (mech / name).write_text("x")
+            os.utime(mech / name, (old, old))
+    stamp = time.time()
+    B._touch(mech / "libhh-aaaa.so")
+    B._touch(mech / "libgroup_soma-cccc.so")
+    assert B.prune_stale(stamp) == 3
+    assert sorted(p.name for p in mech.iterdir()) == sorted(
+        ["libhh-aaaa.so", "hh-aaaa.cu", "hh-aaaa.log", "libgroup_soma-cccc.so", "group_soma-cccc.cu",
+         "group_soma-cccc.log"])

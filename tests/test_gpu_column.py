@@ -125,3 +125,31 @@ def test_two_process_column_shards(tmp_path):
     whole = ColumnShard(spec, 0, n_cells)
     whole.launch(steps)
     np.testing.assert_allclose(table[0][:, 1] + table[1][:, 1], whole.checksums()[:, 1], rtol=1e-12)
+
+
+@pytest.mark.parametrize("bench_options", [False, True])
+def test_errors_inside_the_soma_group_match_the_sequential_schedule(bench_options):
+    """A soma population that fails inside the grouped launch (conductances
+    so large that its current overflows for two cells) reports exactly the
+    error the one-stream schedule reports (member status words, instance in
+    caller order)."""
+    from paper_1905_02241_b200.column import ColumnShard, ColumnSpec, host_stores
+    from paper_1905_02241_b200.runner import InterpError
+
+    spec = ColumnSpec(n_cells=400, dend_per_cell=3, syn_per_cell=5, seed=11)
+    opts = None
+    if bench_options:
+        from bench import options_for as opts
+    msgs = {}
+    for schedule in ("sequential", "grouped"):
+        host = host_stores(spec, 0, spec.n_cells)
+        host["NaTs2_t"].arrays["gNaTs2_tbar"][[123, 45]] = 1e308
+        host["NaTs2_t"].arrays["ena"][[123, 45]] = -1e300  # ina = g m^3 h (v - ena) overflows
+        shard = ColumnShard(spec, 0, spec.n_cells, opts, schedule=schedule, host=host)
+        assert shard.schedule == schedule
+        shard.launch(3)
+        with pytest.raises(InterpError) as e:
+            shard.check()
+        msgs[schedule] = str(e.value)
+    assert msgs["grouped"] == msgs["sequential"]
+    assert "instance 45 " in msgs["sequential"], msgs

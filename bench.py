@@ -21,6 +21,8 @@ BASELINE.json configs:
                           20M instances / GPU split evenly (6 launches / step)
   kinetic1m   configs[3]  6-state KINETIC Na (runtime LU k=6) + cdp5-style
                           Newton k=5 with LU, 1M instances each
+  kinetic10m  the same kernels at 10M instances each (inputs >> L2): where
+                          the 1M launch-size floor does not bind
   column      configs[4]  100k-cell synthetic column, cells split over ranks
                           (strong scaling)
 
@@ -77,6 +79,8 @@ WORKLOADS = {
         "couplings": [("cadyn", "ica", "Ca_HVA", "ica")],
     },
     "kinetic1m": {"config": BASELINE["configs"][3], "mechs": [("na6", 1_000_000), ("cdp5ish", 1_000_000)], "nodes": 0},
+    "kinetic10m": {"config": BASELINE["configs"][3] + " -- at 10M instances each (inputs >> L2)",
+                   "mechs": [("na6", 10_000_000), ("cdp5ish", 10_000_000)], "nodes": 0},
     # configs[4]: strong scaling -- the column is fixed, cells are split over ranks
     "column": {"config": BASELINE["configs"][4], "mechs": [], "nodes": 0, "cells": 100_000},
 }
@@ -1011,7 +1015,7 @@ def main():
         e2e = None if args.no_e2e else e2e_measure(args.workload, dist)
     also = {}
     if not args.no_also and not column:
-        for other in ("hh1m", "hh10m", "bbp20m", "kinetic1m"):
+        for other in ("hh1m", "hh10m", "bbp20m", "kinetic1m", "kinetic10m"):
             if other == args.workload:
                 continue
             # warm-up past the initial transient: Newton iteration counts

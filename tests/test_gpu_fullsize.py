@@ -137,15 +137,24 @@ def test_bbp_set_permutation_invariance():
             np.testing.assert_array_equal(out.arrays[k][inv], gpu.arrays[k], err_msg=f"{stem}:{k}")
 
 
-def test_kinetic_1m_prefix():
+_KINETIC_REF = {}
+
+
+@pytest.mark.parametrize("n", [1_000_000, 10_000_000])
+def test_kinetic_prefix(n):
+    """kinetic1m and kinetic10m as bench.py runs them (1000 steps, bench
+    builds): the first 65,536 instances vs the oracle (computed once)."""
     from paper_1905_02241_b200.instance import init
     from paper_1905_02241_b200.runner import CudaRunner, simulate
 
     for stem in ("na6", "cdp5ish"):
         ir = load_ir(stem)
-        gpu = simulate(ir, init(ir, 1_000_000, 42), 1000, runner=_runner(stem, ir))
-        ref = oracle_prefix([stem], PREFIX, 1000, 42)[stem]
+        gpu = simulate(ir, init(ir, n, 42), 1000, runner=_runner(stem, ir))
+        if stem not in _KINETIC_REF:
+            _KINETIC_REF[stem] = oracle_prefix([stem], PREFIX, 1000, 42)[stem]
+        ref = _KINETIC_REF[stem]
         dev, where = parity(ir, ref, _prefix(gpu, PREFIX))
-        assert dev <= TOL, (stem, dev, where)
+        assert dev <= TOL, (stem, n, dev, where)
         if stem == "cdp5ish":
             assert gpu.newton_iters and max(gpu.newton_iters) <= 50
+        del gpu

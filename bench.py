@@ -756,7 +756,8 @@ def e2e_measure(name, dist, calls=2, timesteps=1000):
     h2d = int(sum(_h2d(j) for j in jobs))
     d2h = int(sum(_d2h(j) for j in jobs))
     return _e2e_line(n_all * timesteps * calls / dt, h2d, d2h, timesteps, calls,
-                     f"one public-API call (runner.simulate{'_nodes' if w['nodes'] else ''}): pinned H2D of the store"
+                     f"one public-API call (runner.simulate{'_nodes' if w['nodes'] else ''}): pinned H2D of the store "
+                     "(arrays no kernel touches stay on the host, scanned for non-finite values there)"
                      + (", node_index + node_v upload, device sort" if w["nodes"] else "")
                      + f", nrn_init, {timesteps} timesteps, D2H of the written arrays"
                      + (" and node rhs/d" if w["nodes"] else ""),
@@ -777,11 +778,16 @@ def _e2e_line(value, h2d_call, d2h_call, timesteps, calls, step, phases=None):
 
 
 def _h2d(job):
-    """Bytes the public call copies host->device: the whole store (v excepted
-    in node mode: it is gathered from the node voltages; i_acc/g_acc are
-    outputs only), node_index, node_v."""
+    """Bytes the public call copies host->device: the store (v excepted in
+    node mode: it is gathered from the node voltages; i_acc/g_acc are
+    outputs only; arrays no kernel reads or writes stay on the host,
+    runner._unread_arrays), node_index, node_v."""
+    from paper_1905_02241_b200.runner import _unread_arrays
+
     ir, runner, data, extra, _, n = job
-    b = sum(a.nbytes for k, a in data.arrays.items() if not (extra is not None and k == "v"))
+    unread = set(_unread_arrays(runner, data, ("initialize", "step_nodes" if extra is not None else "step")))
+    b = sum(a.nbytes for k, a in data.arrays.items()
+            if not (extra is not None and k == "v") and k not in unread)
     if extra is not None:
         b += extra[0].nbytes + extra[1].nbytes
     return b

@@ -821,13 +821,56 @@ class PopulationGroup:
                 r.check(dev)
 
 
-def simulate(layout, data, steps: int, jac_mode: str = "exact", on_step=None, runner: CudaRunner | None = None):
+def _unread_arrays(runner: "CudaRunner", data, kernels) -> list[str]:
+    """Arrays of `data` that none of `kernels` reads or writes (parameters the
+    mechanism declares but never uses): their values never reach the device
+    and never come back, so a call need not upload them -- only their
+    finiteness matters (the reference scans every array after every kernel,
+    interp.py:538-545).  Written arrays are always uploaded: a conditional
+    write must leave the other instances' values as they were."""
+    touched = set()
+    for k in kernels:
+        touched |= set(runner.abi.kernels[k]["loads"]) | set(runner.abi.kernels[k]["stores"])
+    return [n for n in data.arrays if n not in touched and n != "v"]
+
+
+class _HostScan:
+    """First non-finite index of host arrays, on a worker thread (numpy
+    releases the GIL) while the device steps."""
+
+    def __init__(self, arrays: dict):
+        import threading
+
+        self.arrays = arrays
+        self.bad: dict[str, int] = {}
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+
+    def _run(self) -> None:
+        for name, a in self.arrays.items():
+            if not np.isfinite(a).all():
+                self.bad[name] = int(np.flatnonzero(~np.isfinite(a))[0])
+
+    def join(self) -> dict:
+        self.thread.join()
+        return self.bad
+
+
+def simulate(layout, data, steps: int, jac_mode: str = "exact", on_step=None, runner: CudaRunner | None = None,
+             _skip_unread: bool = True):
     """GPU twin of modlc.interp.simulate (interp.py:640-655): one upload,
     initialize, `steps` fused state+current launches, one download."""
     runner = runner or CudaRunner(layout, jac_mode=jac_mode)
     # i_acc / g_acc are outputs only (written with `=` by nrn_cur, read by
-    # nothing): not uploaded; downloaded once a launch has written them
-    dev = runner.to_device(data, skip=("i_acc", "g_acc"))
+    # nothing): not uploaded; downloaded once a launch has written them.
+    # Arrays no kernel reads are not uploaded either; a host thread checks
+    # them for non-finite values while the device steps, and if it finds one
+    # the call is redone with the whole store (the reference reports it after
+    # the first kernel).
+    unread = _unread_arrays(runner, data, ("initialize", "step")) if (_skip_unread and on_step is None) else []
+    scan = _HostScan({n: data.arrays[n] for n in unread}) if unread else None
+    dev = runner.to_device(data, skip=("i_acc", "g_acc") + tuple(unread))
+    err = None
     try:
         runner.run_kernel(dev, "initialize", 1)
         if on_step is None:
@@ -837,14 +880,19 @@ def simulate(layout, data, steps: int, jac_mode: str = "exact", on_step=None, ru
                 runner.run_kernel(dev, "step", 1)
                 runner.to_host(dev, data, only_dirty=True)
                 on_step(step, data)
-    finally:
-        runner.to_host(dev, data, only_dirty=True)
+    except InterpError as exc:
+        err = exc
+    if scan is not None and scan.join():
+        return simulate(layout, data, steps, jac_mode, on_step, runner, _skip_unread=False)
+    runner.to_host(dev, data, only_dirty=True)
+    if err is not None:
+        raise err
     return data
 
 
 def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, node_d=None,
                    jac_mode: str = "exact", runner: CudaRunner | None = None, timings: dict | None = None,
-                   reset: bool = True):
+                   reset: bool = True, _skip_unread: bool = True):
     """node_index run of one mechanism population (builder extension).
 
     Per timestep: v_i = node_v[node_index[i]]; nrn_state; nrn_cur; then
@@ -871,8 +919,11 @@ def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, 
         node_rhs = node_d = None
     prep = runner.prepare_nodes(int(data.n), node_index, node_v, node_rhs, node_d, stream=aux)
     # v is never uploaded (every instance's voltage is its node's); i_acc /
-    # g_acc are outputs only
-    dev = runner.to_device(data, skip=("v", "i_acc", "g_acc"))
+    # g_acc are outputs only; arrays no kernel reads are scanned on the host
+    # instead (see simulate)
+    unread = _unread_arrays(runner, data, ("initialize", "step_nodes")) if _skip_unread else []
+    scan = _HostScan({n: data.arrays[n] for n in unread}) if unread else None
+    dev = runner.to_device(data, skip=("v", "i_acc", "g_acc") + tuple(unread))
     t["upload"] = clock() - t0
     t0 = clock()
     nb = runner.bind_nodes(dev, node_index, prepared=prep)
@@ -883,6 +934,7 @@ def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, 
         # first instance (in caller order) that reads it
         dev.prebad["v"] = int(np.flatnonzero(~np.isfinite(node_v[np.asarray(node_index)]))[0])
     t["bind_nodes"] = clock() - t0
+    err = None
     try:
         t0 = clock()
         runner.run_kernel(dev, "initialize", 1)
@@ -890,16 +942,22 @@ def simulate_nodes(layout, data, steps: int, node_index, node_v, node_rhs=None, 
         t0 = clock()
         runner.run_kernel(dev, "step_nodes", steps)
         t["steps"] = clock() - t0
-    finally:
-        t0 = clock()
-        runner.to_host(dev, data, only_dirty=True)
-        out = {}
-        for name in ("node_rhs", "node_d"):
-            arr = np.empty(nb.n_nodes)
-            rt.d2h(arr.ctypes.data, getattr(nb, name), arr.nbytes, runner.stream)
-            out[name] = arr
-        runner.stream.sync()
-        t["download"] = clock() - t0
+    except InterpError as exc:
+        err = exc
+    if scan is not None and scan.join():
+        return simulate_nodes(layout, data, steps, node_index, node_v, node_rhs, node_d, jac_mode, runner, timings,
+                              reset, _skip_unread=False)
+    t0 = clock()
+    runner.to_host(dev, data, only_dirty=True)
+    out = {}
+    for name in ("node_rhs", "node_d"):
+        arr = np.empty(nb.n_nodes)
+        rt.d2h(arr.ctypes.data, getattr(nb, name), arr.nbytes, runner.stream)
+        out[name] = arr
+    runner.stream.sync()
+    t["download"] = clock() - t0
+    if err is not None:
+        raise err
     if timings is not None:
         timings.update(t)
     return data, out["node_rhs"], out["node_d"]

@@ -254,3 +254,50 @@ def test_step_unique_kernel(stem, sparse):
     dev, where = parity(ir, ref, a)
     assert dev <= TOL, (where, dev)
     _check_nodes(rhs_a, d_a, rhs_ref, d_ref, terms)
+
+
+def test_unused_arrays_are_not_uploaded_but_still_checked():
+    """simulate_nodes leaves arrays no kernel reads or writes (the synapse's
+    Use, Dep, Fac, u0, Nrrp) on the host -- same results bit for bit as the
+    whole-store upload -- and a non-finite value in one of them still raises
+    the oracle's error (found by the host scan, the call is redone with the
+    whole store)."""
+    from paper_1905_02241_b200.runner import CudaRunner, InterpError, _unread_arrays, simulate_nodes
+
+    ir = load_ir("ProbAMPANMDA_EMS")
+    n, n_nodes = 20_000, 3_000
+    idx, nv = _inputs(n, n_nodes, 12)
+    r = CudaRunner(ir)
+    assert set(_unread_arrays(r, O.init(ir, 8, 1), ("initialize", "step_nodes"))) == {"Use", "Dep", "Fac", "u0", "Nrrp"}
+    a, rhs_a, d_a = simulate_nodes(ir, O.init(ir, n, 2), 50, idx, nv, runner=r)
+    b, rhs_b, d_b = simulate_nodes(ir, O.init(ir, n, 2), 50, idx, nv, runner=r, _skip_unread=False)
+    for k in a.arrays:
+        np.testing.assert_array_equal(a.arrays[k].view(np.int64), b.arrays[k].view(np.int64), err_msg=k)
+    np.testing.assert_array_equal(rhs_a.view(np.int64), rhs_b.view(np.int64))
+    np.testing.assert_array_equal(d_a.view(np.int64), d_b.view(np.int64))
+    bad = O.init(ir, n, 2)
+    bad.arrays["Dep"][777] = np.inf
+    with pytest.raises(Exception) as want:
+        N.simulate_nodes(ir, bad.copy(), 5, idx, nv)
+    with pytest.raises(InterpError) as got:
+        simulate_nodes(ir, bad.copy(), 5, idx, nv, runner=r)
+    assert str(got.value) == str(want.value)
+    assert "'Dep'" in str(got.value)
+
+
+def test_simulate_skips_unused_arrays_the_same_way():
+    from paper_1905_02241_b200.runner import CudaRunner, InterpError, simulate
+
+    ir = load_ir("ProbAMPANMDA_EMS")
+    r = CudaRunner(ir)
+    a = simulate(ir, O.init(ir, 5000, 3), 40, runner=r)
+    b = simulate(ir, O.init(ir, 5000, 3), 40, runner=r, _skip_unread=False)
+    for k in a.arrays:
+        np.testing.assert_array_equal(a.arrays[k].view(np.int64), b.arrays[k].view(np.int64), err_msg=k)
+    bad = O.init(ir, 5000, 3)
+    bad.arrays["u0"][4321] = np.nan
+    with pytest.raises(Exception) as want:
+        O.simulate(ir, bad.copy(), 5)
+    with pytest.raises(InterpError) as got:
+        simulate(ir, bad.copy(), 5, runner=r)
+    assert str(got.value) == str(want.value)

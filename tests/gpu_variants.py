@@ -59,6 +59,10 @@ def variants():
         out.append((st, dict(fmad=True)))
     for ilp in (1, 2):
         out.append(("corpus_exp2syn", dict(fast_path=True, fast_redo=True, pipe=True, ilp=ilp)))
+    for kw in (dict(exp_share=True, fast_redo=True, pipe=True, ilp=2),
+               dict(exp_share=True, recip=True, fast_path=False, grid_waves=0),
+               dict(exp_share=True, fast_redo=True, pipe=True, pdl=True)):
+        out.append(("rwglobal", kw))
     for st, kw in FALLBACK_BENCH:
         out.append((st, kw))
     for st in RELAXED_STEMS:

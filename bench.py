@@ -19,6 +19,7 @@ BASELINE.json configs:
                           same kernel where the 1M size floor does not bind
   bbp20m      configs[2]  NaTs2_t, K_Pst, Ca_HVA, SKv3_1, Ih, CaDynamics_E2;
                           20M instances / GPU split evenly (6 launches / step)
+  bbp20m_grouped          the same step as ONE population-group launch
   kinetic1m   configs[3]  6-state KINETIC Na (runtime LU k=6) + cdp5-style
                           Newton k=5 with LU, 1M instances each
   kinetic10m  the same kernels at 10M instances each (inputs >> L2): where
@@ -77,6 +78,15 @@ WORKLOADS = {
         # CaDynamics_E2 accumulates the calcium current Ca_HVA writes (same
         # compartments, same order): its `ica` slot is Ca_HVA's array
         "couplings": [("cadyn", "ica", "Ca_HVA", "ica")],
+    },
+    # the same six populations stepped by ONE population-group launch per
+    # timestep (codegen_cuda.emit_group kind="direct"; bit-identical)
+    "bbp20m_grouped": {
+        "config": BASELINE["configs"][2] + " -- all six populations in one launch per step",
+        "mechs": [(m, 20_000_000 // 6) for m in ("NaTs2_t", "K_Pst", "Ca_HVA", "SKv3_1", "Ih", "cadyn")],
+        "nodes": 0,
+        "couplings": [("cadyn", "ica", "Ca_HVA", "ica")],
+        "grouped": True,
     },
     "kinetic1m": {"config": BASELINE["configs"][3], "mechs": [("na6", 1_000_000), ("cdp5ish", 1_000_000)], "nodes": 0},
     "kinetic10m": {"config": BASELINE["configs"][3] + " -- at 10M instances each (inputs >> L2)",
@@ -436,12 +446,15 @@ def run_workload(name, args, dist, sustained=True):
     s0 = pops[0].runner.stream
     for p in pops:  # one stream: launch order == step order (bbp20m's coupling)
         p.runner.stream = s0
+    members = list(pops)
+    if w.get("grouped"):
+        pops = [_DirectGroup(pops, w.get("couplings", ()), s0)]
     K, W = args.steps, args.warmup
     for _ in range(W):
         for p in pops:
             p.launch(1)
     s0.sync()
-    for p in pops:
+    for p in members:
         p.runner.check(p.dev)
     # the timed graph: K steps.  External event records before a step and
     # after every population's launch time each kernel inside this replay:
@@ -484,7 +497,7 @@ def run_workload(name, args, dist, sustained=True):
     else:
         per_pop_ms = [total_ms]
     del graph
-    for p in pops:
+    for p in members:
         p.runner.check(p.dev)
     clocks = clk.summary()
     sus = None
@@ -501,7 +514,7 @@ def run_workload(name, args, dist, sustained=True):
             ev_b.sync()
         sms = ev_a.elapsed_ms(ev_b)
         del g2
-        for p in pops:
+        for p in members:
             p.runner.check(p.dev)
         smax = dist.allreduce([sms], "max")[0]
         n_all_s = dist.allreduce([float(sum(p.n for p in pops))], "sum")[0]
@@ -517,19 +530,18 @@ def run_workload(name, args, dist, sustained=True):
     dom = pops[j]
     sm_mhz = clocks.get("sm_mhz")
     key = f"{dom.build_key}@{dom.n}"
-    roof = _roofline(dom.kernel_name, dom.launch_bytes(), _fp64_instr(dom.ir, dom.n, key), per_pop_ms[j] / K, [key],
-                     sm_mhz)
+    roof = _roofline(dom.kernel_name, dom.launch_bytes(), _pop_fp64(dom), per_pop_ms[j] / K, [key], sm_mhz)
     roof["share_of_step"] = per_pop_ms[j] / max(total_ms, 1e-30)
     roof["model"] = _describe(dom)
     from paper_1905_02241_b200.parallel import device_checksums
 
-    local = np.concatenate([device_checksums(p.runner, p.dev) for p in pops])
+    local = np.concatenate([device_checksums(p.runner, p.dev) for p in members])
     table = dist.allgather(local)
     per_mech = {}
     for i, p in enumerate(pops):
         ms = per_pop_ms[i] / K
         key = f"{p.build_key}@{p.n}"
-        r = _roofline(p.kernel_name, p.launch_bytes(), _fp64_instr(p.ir, p.n, key), ms, [key], sm_mhz)
+        r = _roofline(p.kernel_name, p.launch_bytes(), _pop_fp64(p), ms, [key], sm_mhz)
         per_mech[p.stem] = {"instances": p.n, "ms_per_launch": ms, "GBps": r["achieved"], "hbm_frac": r["frac"],
                             "fp64_frac": r["fp64"]["frac"], "bound": r["bound"], "traffic": r["traffic"],
                             "bytes_per_instance_step": p.launch_bytes() / p.n, "build": p.build_key}
@@ -546,6 +558,60 @@ def run_workload(name, args, dist, sustained=True):
         "roofline": roof,
         "per_mechanism": per_mech,
     }
+
+
+def _pop_fp64(p):
+    """FP64 instructions of one launch of a population (or of a direct group:
+    the sum over its members, each counted with its own build's ncu count)."""
+    if isinstance(p, _DirectGroup):
+        parts = [_pop_fp64(m) for m in p.pops]
+        return sum(x for x, _ in parts), "; ".join(sorted({c for _, c in parts}))
+    return _fp64_instr(p.ir, p.n, f"{p.build_key}@{p.n}")
+
+
+class _DirectGroup:
+    """Every population of a direct workload as ONE population-group launch
+    per step (runner.PopulationGroup kind="direct": every CTA runs every
+    population in turn; an ion consumer follows its producer with the
+    producer's ilp, so each thread reads the ica it just wrote)."""
+
+    def __init__(self, pops, couplings, stream):
+        import dataclasses
+
+        from paper_1905_02241_b200.runner import PopulationGroup
+
+        by = {p.stem: p for p in pops}
+        chained = {dst: src for dst, _, src, _ in couplings}
+        chains = []
+        for p in pops:
+            if p.stem in chained:
+                continue
+            chain = [(p.runner, p.dev)]
+            for dst, src in chained.items():
+                if src == p.stem:
+                    q = by[dst]
+                    chain.append((q.runner, q.dev, dataclasses.replace(q.runner.options, ilp=p.runner.options.ilp)))
+            chains.append(chain)
+        self.group = PopulationGroup("bbp", chains, kind="direct")
+        self.pops = pops
+        self.stream = stream
+        self.n = sum(p.n for p in pops)
+        self.stem = "group(" + "+".join(p.stem for p in pops) + ")"
+        self.kernel = "step"
+        self.ir = pops[0].ir
+        self.build_key = self.group.gb.so_path.stem[3:]
+        self.runner = pops[0].runner
+        self.dev = pops[0].dev
+
+    @property
+    def kernel_name(self):
+        return f"{self.group.gb.symbol}_k_step_group"
+
+    def launch(self, steps=1):
+        self.group.launch(self.stream, steps)
+
+    def launch_bytes(self):
+        return sum(p.launch_bytes() for p in self.pops)
 
 
 def _describe(pop):
@@ -1021,7 +1087,7 @@ def main():
         e2e = None if args.no_e2e else e2e_measure(args.workload, dist)
     also = {}
     if not args.no_also and not column:
-        for other in ("hh1m", "hh10m", "bbp20m", "kinetic1m", "kinetic10m"):
+        for other in ("hh1m", "hh10m", "bbp20m", "bbp20m_grouped", "kinetic1m", "kinetic10m"):
             if other == args.workload:
                 continue
             # warm-up past the initial transient: Newton iteration counts

@@ -175,12 +175,12 @@ class GroupBuild:
         self.text = text
 
 
-def build_group(name: str, chains, fmad: bool = False, force: bool = False) -> GroupBuild:
+def build_group(name: str, chains, fmad: bool = False, force: bool = False, kind: str = "unique") -> GroupBuild:
     """emit_group + nvcc -> content-addressed shared object (same keying as
     build_mechanism: generated text, portable flags, header digest)."""
     from .codegen_cuda import _cname, emit_group
 
-    unit, abis = emit_group(name, chains)
+    unit, abis = emit_group(name, chains, kind)
     flags = base_flags(fmad)
     portable = [f for f in flags if not f.startswith("-I")]
     key = hashlib.sha256((unit.text + "\0" + " ".join(portable) + "\0" + _headers_digest()).encode()).hexdigest()[:20]

@@ -766,11 +766,18 @@ class PopulationGroup:
     generated code as its standalone kernel, so results are bit-identical.
     Errors are reported through the members' runners (`check`)."""
 
-    def __init__(self, name: str, chains):
+    def __init__(self, name: str, chains, kind: str = "unique"):
+        """kind="direct": direct (no node_index) populations, each running its
+        fused step kernel's code; members may be (runner, dev, options) to
+        build a member with other launch options than its runner (chained
+        direct members need one ilp).  Every CTA of the resident grid runs
+        every member in turn."""
         from .build import build_group
 
         self.name = name
-        self.chains = [list(ch) for ch in chains]
+        self.kind = kind
+        self.chains = [[tuple(m[:2]) for m in ch] for ch in chains]
+        member_opts = [[(m[0].ir, m[2] if len(m) > 2 else m[0].options) for m in ch] for ch in chains]
         runners = [r for ch in self.chains for r, _ in ch]
         if not runners:
             raise ValueError("empty population group")
@@ -779,9 +786,10 @@ class PopulationGroup:
             raise ValueError("population group members need one Jacobian mode")
         self.flags = flags.pop()
         self.device = runners[0].device
-        self.gb = build_group(name, [[(r.ir, r.options) for r, _ in ch] for ch in self.chains])
+        self.gb = build_group(name, member_opts, kind=kind)
         self.lib = C.CDLL(str(self.gb.so_path))
         g = self.gb.symbol
+        self.ilp = {ci: (ch[0][2].ilp if len(ch[0]) > 2 else ch[0][0].options.ilp) for ci, ch in enumerate(chains)}
         fields = [(f"md{ci}_{mi}", r.Struct) for ci, ch in enumerate(self.chains) for mi, (r, _) in enumerate(ch)]
         fields.append(("cta", C.c_longlong * (len(self.chains) + 1)))
         self.Args = type(f"{g}_args", (C.Structure,), {"_fields_": fields})
@@ -789,21 +797,37 @@ class PopulationGroup:
         size_fn.restype = C.c_longlong
         if size_fn() != C.sizeof(self.Args):
             raise RuntimeError(f"ABI mismatch for group {g}: C {size_fn()} vs ctypes {C.sizeof(self.Args)}")
-        self.fn = getattr(self.lib, f"{g}_step_unique")
+        self.fn = getattr(self.lib, f"{g}_step_unique" if kind == "unique" else f"{g}_step_group")
         self.fn.restype = C.c_int
         self.fn.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int]
         self.block = runners[0].options.block
+        self.ctas = None
+        if kind == "direct":
+            f = getattr(self.lib, f"{g}_group_ctas")
+            f.restype = C.c_int
+            rt.set_device(self.device)
+            self.ctas = max(1, int(f()))
+
+    def _chain_ctas(self) -> list[int]:
+        if self.kind == "unique":  # one instance per thread, as many CTAs as that takes
+            return [(max(dev.n for _, dev in ch) + self.block - 1) // self.block for ch in self.chains]
+        # direct: every CTA of the persistent grid runs every member in turn
+        need = max((max(dev.n for _, dev in ch) + self.ilp[ci] * self.block - 1) // (self.ilp[ci] * self.block)
+                   for ci, ch in enumerate(self.chains))
+        return [0] * (len(self.chains) - 1) + [max(1, min(self.ctas, need))]
 
     def args(self):
         vals = []
-        cta = [0]
         for ch in self.chains:
             for r, dev in ch:
-                if dev.nodes is None or dev.nodes.seg_unique not in (1, 2):
+                if self.kind == "unique" and (dev.nodes is None or dev.nodes.seg_unique not in (1, 2)):
                     raise ValueError(f"{r.mb.symbol}: group members need a one-instance-per-node binding")
+                if self.kind == "direct" and dev.nodes is not None:
+                    raise ValueError(f"{r.mb.symbol}: direct group members must not be node-bound")
                 vals.append(r._struct(dev))
-            n = max(dev.n for _, dev in ch)
-            cta.append(cta[-1] + (n + self.block - 1) // self.block)
+        cta = [0]
+        for c in self._chain_ctas():
+            cta.append(cta[-1] + c)
         return self.Args(*vals, (C.c_longlong * len(cta))(*cta))
 
     def launch(self, stream: "rt.Stream", steps: int = 1) -> None:
@@ -811,7 +835,7 @@ class PopulationGroup:
         a = self.args()
         for ch in self.chains:
             for r, dev in ch:
-                dev.dirty |= r._writes["step_nodes"]
+                dev.dirty |= r._writes["step_nodes" if self.kind == "unique" else "step"]
         rt.set_device(self.device)
         rt.check(self.fn(C.byref(a), int(steps), C.c_void_p(stream.handle), self.flags), f"launch group {self.name}")
 

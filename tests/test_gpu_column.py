@@ -153,3 +153,55 @@ def test_errors_inside_the_soma_group_match_the_sequential_schedule(bench_option
         msgs[schedule] = str(e.value)
     assert msgs["grouped"] == msgs["sequential"]
     assert "instance 45 " in msgs["sequential"], msgs
+
+
+def test_direct_population_group_is_bit_identical():
+    """kind="direct" population group: the BBP set (NaTs2_t | K_Pst |
+    Ca_HVA -> CaDynamics_E2 on the shared ica | SKv3_1 | Ih) stepped by ONE
+    launch per timestep gives exactly the six separate launches' results."""
+    import dataclasses
+
+    from bench import options_for
+    from paper_1905_02241_b200.instance import init
+    from paper_1905_02241_b200.runner import CudaRunner, PopulationGroup
+    from conftest import load_ir
+
+    stems = ["NaTs2_t", "K_Pst", "Ca_HVA", "SKv3_1", "Ih", "cadyn"]
+    n, steps = 50_001, 40
+    outs = []
+    for grouped in (False, True):
+        rs, ds = {}, {}
+        for m in stems:
+            ir = load_ir(m)
+            rs[m] = CudaRunner(ir, options=options_for(m))
+            ds[m] = rs[m].to_device(init(ir, n, 7))
+            rs[m].run_kernel(ds[m], "initialize", 1)
+        rs["cadyn"].share_slot(ds["cadyn"], "ica", ds["Ca_HVA"], "ica")
+        s = rs[stems[0]].stream
+        for m in stems:
+            rs[m].stream = s
+        if grouped:
+            cad = dataclasses.replace(rs["cadyn"].options, ilp=rs["Ca_HVA"].options.ilp)
+            g = PopulationGroup("bbp_t", [[(rs["NaTs2_t"], ds["NaTs2_t"])], [(rs["K_Pst"], ds["K_Pst"])],
+                                          [(rs["Ca_HVA"], ds["Ca_HVA"]), (rs["cadyn"], ds["cadyn"], cad)],
+                                          [(rs["SKv3_1"], ds["SKv3_1"])], [(rs["Ih"], ds["Ih"])]], kind="direct")
+            g.launch(s, steps)
+        else:
+            for _ in range(steps):
+                for m in stems:
+                    rs[m].launch(ds[m], "step", 1)
+        s.sync()
+        res = {}
+        for m in stems:
+            rs[m].check(ds[m])
+            got = init(load_ir(m), n, 0)
+            rs[m].to_host(ds[m], got)
+            res[m] = got
+        outs.append(res)
+    for m in stems:
+        for k in outs[0][m].arrays:
+            np.testing.assert_array_equal(outs[0][m].arrays[k].view(np.int64), outs[1][m].arrays[k].view(np.int64),
+                                          err_msg=f"{m}:{k}")
+        for k in outs[0][m].acc:
+            np.testing.assert_array_equal(outs[0][m].acc[k].view(np.int64), outs[1][m].acc[k].view(np.int64),
+                                          err_msg=f"{m}:{k}")

@@ -80,11 +80,14 @@ def child(workload: str, out: str) -> None:
         s0 = pops[0].runner.stream
         for p in pops:
             p.runner.stream = s0
+        members = list(pops)
+        if w.get("grouped"):
+            pops = [bench._DirectGroup(pops, w.get("couplings", ()), s0)]
         for _ in range(WARM_FOR.get(workload, WARM) + 1):
             for p in pops:
                 p.launch(1)
         s0.sync()
-        for p in pops:
+        for p in members:
             p.runner.check(p.dev)
         per_step = len(pops)
         for p in pops:
@@ -122,7 +125,7 @@ def parent(out_dir: Path, workloads: list[str]) -> None:
             per_step = {"sequential": 7, "concurrent": 8, "grouped": 4}[bench._column_mode()["schedule"]]
             regex = "regex:_k_step|combine"
         else:
-            per_step = len(bench.WORKLOADS[wl]["mechs"])
+            per_step = 1 if bench.WORKLOADS[wl].get("grouped") else len(bench.WORKLOADS[wl]["mechs"])
             regex = "regex:_k_step"
         rep = out_dir / f"{wl}"
         cmd = ["ncu", "--set", "full", "--import-source", "on", "--clock-control", "none", "-k", regex,

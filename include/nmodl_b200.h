@@ -196,6 +196,9 @@ int nmodl_nccl_allgather_f64(void *comm, const double *send, double *recv, long 
  * `long long cta[n_chains + 1]` (chain c owns CTAs [cta[c], cta[c+1])).
  *
  *   <name>_step_unique     `nsteps` group launches on `s` (0 or cudaError_t)
+ *   <name>_step_group      same for a direct group (kind="direct": every CTA
+ *                          runs every member in turn), <name>_group_ctas()
+ *                          its resident CTAs
  *   <name>_args_size       sizeof(<name>_args)
  */
 #define NMODL_B200_GROUP(name)                                                        \

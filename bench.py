@@ -22,6 +22,7 @@ BASELINE.json configs:
   bbp20m_grouped          the same step as ONE population-group launch
   kinetic1m   configs[3]  6-state KINETIC Na (runtime LU k=6) + cdp5-style
                           Newton k=5 with LU, 1M instances each
+  kinetic1m_grouped       the kinetic pair as ONE population-group launch
   kinetic10m  the same kernels at 10M instances each (inputs >> L2): where
                           the 1M launch-size floor does not bind
   column      configs[4]  100k-cell synthetic column, cells split over ranks
@@ -86,9 +87,11 @@ WORKLOADS = {
         "mechs": [(m, 20_000_000 // 6) for m in ("NaTs2_t", "K_Pst", "Ca_HVA", "SKv3_1", "Ih", "cadyn")],
         "nodes": 0,
         "couplings": [("cadyn", "ica", "Ca_HVA", "ica")],
-        "grouped": True,
+        "grouped": "bbp",
     },
     "kinetic1m": {"config": BASELINE["configs"][3], "mechs": [("na6", 1_000_000), ("cdp5ish", 1_000_000)], "nodes": 0},
+    "kinetic1m_grouped": {"config": BASELINE["configs"][3] + " -- both populations in one launch per step",
+                          "mechs": [("na6", 1_000_000), ("cdp5ish", 1_000_000)], "nodes": 0, "grouped": "kinetic"},
     "kinetic10m": {"config": BASELINE["configs"][3] + " -- at 10M instances each (inputs >> L2)",
                    "mechs": [("na6", 10_000_000), ("cdp5ish", 10_000_000)], "nodes": 0},
     # configs[4]: strong scaling -- the column is fixed, cells are split over ranks
@@ -448,7 +451,7 @@ def run_workload(name, args, dist, sustained=True):
         p.runner.stream = s0
     members = list(pops)
     if w.get("grouped"):
-        pops = [_DirectGroup(pops, w.get("couplings", ()), s0)]
+        pops = [_DirectGroup(pops, w.get("couplings", ()), s0, w["grouped"])]
     K, W = args.steps, args.warmup
     for _ in range(W):
         for p in pops:
@@ -575,7 +578,7 @@ class _DirectGroup:
     population in turn; an ion consumer follows its producer with the
     producer's ilp, so each thread reads the ica it just wrote)."""
 
-    def __init__(self, pops, couplings, stream):
+    def __init__(self, pops, couplings, stream, name):
         import dataclasses
 
         from paper_1905_02241_b200.runner import PopulationGroup
@@ -592,7 +595,7 @@ class _DirectGroup:
                     q = by[dst]
                     chain.append((q.runner, q.dev, dataclasses.replace(q.runner.options, ilp=p.runner.options.ilp)))
             chains.append(chain)
-        self.group = PopulationGroup("bbp", chains, kind="direct")
+        self.group = PopulationGroup(name, chains, kind="direct")
         self.pops = pops
         self.stream = stream
         self.n = sum(p.n for p in pops)
@@ -1087,7 +1090,7 @@ def main():
         e2e = None if args.no_e2e else e2e_measure(args.workload, dist)
     also = {}
     if not args.no_also and not column:
-        for other in ("hh1m", "hh10m", "bbp20m", "bbp20m_grouped", "kinetic1m", "kinetic10m"):
+        for other in ("hh1m", "hh10m", "bbp20m", "bbp20m_grouped", "kinetic1m", "kinetic1m_grouped", "kinetic10m"):
             if other == args.workload:
                 continue
             # warm-up past the initial transient: Newton iteration counts

@@ -205,3 +205,45 @@ def test_direct_population_group_is_bit_identical():
         for k in outs[0][m].acc:
             np.testing.assert_array_equal(outs[0][m].acc[k].view(np.int64), outs[1][m].acc[k].view(np.int64),
                                           err_msg=f"{m}:{k}")
+
+
+def test_direct_group_with_newton_members_is_bit_identical():
+    """The kinetic pair (register LU; Newton with an LU per iteration) as one
+    direct group launch: states and currents equal the separate launches."""
+    from bench import options_for
+    from paper_1905_02241_b200.instance import init
+    from paper_1905_02241_b200.runner import CudaRunner, PopulationGroup
+    from conftest import load_ir
+
+    stems = ["na6", "cdp5ish"]
+    n, steps = 30_011, 60
+    outs = []
+    for grouped in (False, True):
+        rs, ds = {}, {}
+        for m in stems:
+            ir = load_ir(m)
+            rs[m] = CudaRunner(ir, options=options_for(m))
+            ds[m] = rs[m].to_device(init(ir, n, 9))
+            rs[m].run_kernel(ds[m], "initialize", 1)
+        s = rs[stems[0]].stream
+        for m in stems:
+            rs[m].stream = s
+        if grouped:
+            PopulationGroup("kin_t", [[(rs[m], ds[m])] for m in stems], kind="direct").launch(s, steps)
+        else:
+            for _ in range(steps):
+                for m in stems:
+                    rs[m].launch(ds[m], "step", 1)
+        s.sync()
+        res = {}
+        for m in stems:
+            rs[m].check(ds[m])
+            got = init(load_ir(m), n, 0)
+            rs[m].to_host(ds[m], got)
+            res[m] = got
+        outs.append(res)
+    for m in stems:
+        for k in list(outs[0][m].arrays) + ["i_acc", "g_acc"]:
+            a = outs[0][m].acc[k] if k in ("i_acc", "g_acc") else outs[0][m].arrays[k]
+            b = outs[1][m].acc[k] if k in ("i_acc", "g_acc") else outs[1][m].arrays[k]
+            np.testing.assert_array_equal(a.view(np.int64), b.view(np.int64), err_msg=f"{m}:{k}")

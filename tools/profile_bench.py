@@ -34,7 +34,7 @@ sys.path.insert(0, str(ROOT / "tools"))
 WARM = 3
 # bench.py warms the secondary workloads 100 steps (cdp5ish's Newton iteration
 # counts fall over the first ~100 steps after nrn_init): profile the same state
-WARM_FOR = {"kinetic1m": 100, "kinetic10m": 100}
+WARM_FOR = {"kinetic1m": 100, "kinetic10m": 100, "kinetic1m_grouped": 100}
 FP64_OPCODES = ("DFMA", "DMUL", "DADD", "DSETP", "DMNMX")  # the FP64 pipe (paper_1905_02241_b200.analysis)
 
 
@@ -82,7 +82,7 @@ def child(workload: str, out: str) -> None:
             p.runner.stream = s0
         members = list(pops)
         if w.get("grouped"):
-            pops = [bench._DirectGroup(pops, w.get("couplings", ()), s0)]
+            pops = [bench._DirectGroup(pops, w.get("couplings", ()), s0, w["grouped"])]
         for _ in range(WARM_FOR.get(workload, WARM) + 1):
             for p in pops:
                 p.launch(1)

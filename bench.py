@@ -620,6 +620,8 @@ class _DirectGroup:
 def _describe(pop):
     from paper_1905_02241_b200.traffic import describe
 
+    if isinstance(pop, _DirectGroup):
+        return {m.stem: describe(m.runner.abi, m.kernel) for m in pop.pops}
     return describe(pop.runner.abi, pop.kernel)
 
 

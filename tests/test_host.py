@@ -459,3 +459,28 @@ def test_prune_stale_keeps_what_a_build_touched(tmp_path, monkeypatch):
     assert sorted(p.name for p in mech.iterdir()) == sorted(
         ["libhh-aaaa.so", "hh-aaaa.cu", "hh-aaaa.log", "libgroup_soma-cccc.so", "group_soma-cccc.cu",
          "group_soma-cccc.log"])
+
+
+def test_direct_population_group_text():
+    """emit_group(kind="direct"): every member's fused step code as a device
+    function, called in member order by every CTA with a barrier between
+    members (their cp.async pipelines share the dynamic shared memory), a
+    resident-CTA query; chained members must share ilp."""
+    import dataclasses
+
+    from paper_1905_02241_b200.codegen_cuda import CudaOptions, emit_group
+
+    ca = CudaOptions(ilp=2, pipe=True)
+    unit, _ = emit_group("d_grp", [[(load_ir("NaTs2_t"), CudaOptions(ilp=2, pipe=True))],
+                                   [(load_ir("Ca_HVA"), ca), (load_ir("cadyn"), dataclasses.replace(ca))]],
+                         kind="direct")
+    t = unit.text
+    k = t.index("d_grp_k_step_group(const d_grp_args a)")
+    body = t[k:t.index("\n}\n", k)]
+    calls = [ln.strip() for ln in body.splitlines() if "_k_step_dev<JAC_FD>" in ln]
+    assert [c.split("::")[1].split("_k_step_dev")[0] for c in calls] == ["NaTs2_t", "Ca_HVA", "CaDynamics_E2"]
+    assert body.count("__syncthreads();") == 2
+    assert "int d_grp_group_ctas(void)" in t and "int d_grp_step_group(" in t
+    with pytest.raises(ValueError):
+        emit_group("bad", [[(load_ir("Ca_HVA"), CudaOptions(ilp=2)), (load_ir("cadyn"), CudaOptions(ilp=1))]],
+                   kind="direct")

@@ -118,7 +118,8 @@ def options_for(stem: str):
                              exp_share=True, fast_redo=True),  # 0.0717 -> 0.0574 ms
         "Ca_HVA": CudaOptions(ilp=2, min_blocks=2, pipe=True, recip=True, div_approx=True, fast_redo=True),  # 0.0707 -> 0.0561
         "SKv3_1": CudaOptions(ilp=2, grid_waves=4, div_approx=True, fast_redo=True),  # 0.0500 -> 0.0426 -> 0.0388 ms (r02 ilp=2)
-        "Ih": CudaOptions(ilp=2, pipe=True, grid_waves=4, recip=True, div_approx=True, fast_redo=True),  # 0.0474 -> 0.0392 ms
+        "Ih": CudaOptions(ilp=2, pipe=True, grid_waves=4, recip=True, div_approx=True, fast_redo=True,
+                          min_blocks=4),  # 0.0474 -> 0.0392 ms; min_blocks=4: step_unique at 64 registers (column Ih 7.5 -> 6.5 us at 12.5k cells)
         "cadyn": CudaOptions(pipe=True, min_blocks=2),  # 0.0471 -> 0.0462 ms (profiles/r02/tune_small.jsonl)
         "na6": CudaOptions(ilp=1, min_blocks=2, pipe=True, fast_redo=True, lu_spec=True),  # 0.0485 -> 0.0369 ms
         "cdp5ish": CudaOptions(ilp=1, min_blocks=2, pipe=True, div_approx=True, fast_redo=True, lu_spec=True),  # 0.0583 -> 0.0390
@@ -128,7 +129,16 @@ def options_for(stem: str):
     # programmatic dependent launch for every kernel: the next step's CTAs are
     # scheduled while the previous grid drains (column 357 -> 352 us, 12.5k
     # cells 56.3 -> 54.3 us; profiles/r02/pdl_*.json); NMODL_PDL=0 turns it off
-    return dataclasses.replace(tuned.get(stem, CudaOptions()), pdl=os.environ.get("NMODL_PDL", "1") == "1")
+    opts = dataclasses.replace(tuned.get(stem, CudaOptions()), pdl=os.environ.get("NMODL_PDL", "1") == "1")
+    # experiments: NMODL_OPT_<stem>="min_blocks=4,ilp=1" overrides fields of one mechanism's build
+    extra = os.environ.get(f"NMODL_OPT_{stem}")
+    if extra:
+        kw = {}
+        for part in extra.split(","):
+            k, v = part.split("=")
+            kw[k] = (v in ("1", "True", "true")) if isinstance(getattr(opts, k), bool) else int(v)
+        opts = dataclasses.replace(opts, **kw)
+    return opts
 
 
 RELAXED_NOTE = ("fp64 throughout; rate code uses reciprocal/quotient shadows (X/(1/E) -> X*E), <=2-ulp division, "

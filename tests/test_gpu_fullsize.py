@@ -158,3 +158,45 @@ def test_kinetic_prefix(n):
         if stem == "cdp5ish":
             assert gpu.newton_iters and max(gpu.newton_iters) <= 50
         del gpu
+
+
+def test_column_100k_as_bench_runs_it_prefix_matches_oracle():
+    """configs[4] exactly as bench.py runs it (100,000 cells, bench builds,
+    the grouped soma schedule, 1000 steps): cells never interact and every
+    cell's instances, synapse compartments and node voltages are drawn from
+    global ids (column.shard_layout), so the first 150 cells of the full
+    column must equal the 150-cell column -- states, currents and the node
+    rhs/d of those cells' compartments -- against oracle/column_np.py."""
+    from bench import _column_mode, options_for
+    from oracle import column_np as CN
+    from paper_1905_02241_b200.column import (COUPLINGS, LAUNCH_ORDER, ColumnShard, ColumnSpec, load_irs,
+                                              shard_layout)
+    from paper_1905_02241_b200.instance import init_range
+    from parity import node_dev
+
+    full = ColumnSpec(n_cells=100_000)
+    k_cells, steps = 150, 1000
+    shard = ColumnShard(full, 0, full.n_cells, options_for, **_column_mode())
+    shard.launch(steps)
+    shard.check()
+    irs = load_irs()
+    small = ColumnSpec(n_cells=k_cells, dend_per_cell=full.dend_per_cell, syn_per_cell=full.syn_per_cell,
+                       seed=full.seed)
+    lay = shard_layout(small, 0, k_cells)
+    datas = {m: init_range(irs[m], lay["mechs"][m][0], lay["mechs"][m][1], small.seed) for m in LAUNCH_ORDER}
+    datas = {m: O.InstanceData(x.n, x.arrays, x.acc, x.scalars) for m, x in datas.items()}
+    idx = {m: lay["mechs"][m][2] for m in LAUNCH_ORDER}
+    terms = {}
+    ref, rhs, d = CN.simulate_column(irs, datas, idx, lay["node_v"], LAUNCH_ORDER, COUPLINGS, steps, terms=terms)
+    for m in LAUNCH_ORDER:
+        lo, hi, _ = shard.layout["mechs"][m]
+        got = init_range(irs[m], lo, hi, full.seed)
+        shard.runners[m].to_host(shard.devs[m], got)
+        k = lay["mechs"][m][1]  # the small column's instance count of m
+        dev, where = parity(irs[m], ref[m], _prefix(got, k))
+        assert dev <= TOL, (m, dev, where)
+        del got
+    nodes = shard.nodes.download(shard.stream)
+    nn = k_cells * full.nodes_per_cell
+    for name, want, scale in (("node_rhs", rhs, terms["rhs"]), ("node_d", d, terms["d"])):
+        assert node_dev(nodes[name][:nn], want, scale) <= 1e-10, name

@@ -283,8 +283,11 @@ class ColumnShard:
             for e in joins:
                 rt.stream_wait(main, e)
             self._combine_soma(L, C)
-            for stem in after:
-                self.runners[stem].launch(self.devs[stem], "step_nodes", 1)
+            for k, stem in enumerate(after):
+                # the first population after the combine reads nothing the combine
+                # writes except the node rhs/d it folds into: its loads and maths
+                # may start while the combine runs (programmatic late wait)
+                self.runners[stem].launch(self.devs[stem], "step_nodes", 1, late_wait=(k == 0))
 
     def kernels_per_step(self) -> int:
         """Our kernels per timestep (memsets not counted)."""

@@ -433,15 +433,21 @@ class CudaRunner:
             return "step_unique"
         return "step_nodes"
 
-    def launch(self, dev: DeviceInstanceData, kernel_name: str, steps: int = 1, newton_rec: int = 0) -> None:
-        """Enqueue `steps` launches on the runner's stream (no sync, no checks)."""
+    def launch(self, dev: DeviceInstanceData, kernel_name: str, steps: int = 1, newton_rec: int = 0,
+               late_wait: bool = False) -> None:
+        """Enqueue `steps` launches on the runner's stream (no sync, no checks).
+        `late_wait` (tiled node kernel of a pdl build): the kernel's programmatic
+        wait moves from its start to its node fold -- only for a launch whose
+        predecessor in the stream writes nothing this population reads but the
+        node arrays (ColumnShard: the synapses after the soma combine)."""
         if kernel_name == "step_nodes" and dev.nodes is None:
             raise ValueError("step_nodes needs bind_nodes() first")
         md = self._struct(dev, newton_rec)
         dev.dirty |= self._writes[kernel_name]
         rt.set_device(self.device)
         entry = self.entry[self.node_kernel(dev) if kernel_name == "step_nodes" else kernel_name]
-        rc = entry(C.byref(md), int(steps), C.c_void_p(self.stream.handle), self.flags)
+        flags = self.flags | (2 if (late_wait and kernel_name == "step_nodes") else 0)
+        rc = entry(C.byref(md), int(steps), C.c_void_p(self.stream.handle), flags)
         rt.check(rc, f"launch {self.mb.symbol}_{kernel_name}")
 
     def run_kernel(self, data, kernel_name: str, steps: int = 1):

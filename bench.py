@@ -891,7 +891,9 @@ def e2e_column(dist, calls=1, timesteps=1000):
     """configs[4] through the public column call (column.simulate_column):
     pinned H2D of this rank's seven stores, the node voltages and node_index
     arrays, the device-side node layout, nrn_init, `timesteps` steps of all
-    populations, D2H of every written array and the node arrays."""
+    populations, D2H of every written array and the node arrays.  The
+    inputs (stores, node_index, node_v) are generated before the clock
+    starts."""
     from paper_1905_02241_b200 import runtime as rt
     from paper_1905_02241_b200.column import LAUNCH_ORDER, host_stores, shard_layout, simulate_column
     from paper_1905_02241_b200.parallel import partition_cells
@@ -904,7 +906,7 @@ def e2e_column(dist, calls=1, timesteps=1000):
     lay = shard_layout(spec, lo, hi)
     mode = _column_mode()
     # warm-up call: loads the kernels (reused below), primes the caches
-    _, _, shard = simulate_column(spec, 10, lo, hi, host=host, options_for=options_for, **mode)
+    _, _, shard = simulate_column(spec, 10, lo, hi, host=host, options_for=options_for, layout=lay, **mode)
     runners = shard.runners
     writes = {m: runners[m]._writes["initialize"] | runners[m]._writes["step_nodes"] | {"v"} for m in LAUNCH_ORDER}
     del shard
@@ -914,7 +916,7 @@ def e2e_column(dist, calls=1, timesteps=1000):
     t0 = time.perf_counter()
     for _ in range(calls):
         _, nodes, shard = simulate_column(spec, timesteps, lo, hi, host=host, options_for=options_for,
-                                          runners=runners, **mode)
+                                          runners=runners, layout=lay, **mode)
     dt = time.perf_counter() - t0
     dt = dist.allreduce([dt], "max")[0]
     n_rank = sum(h.n for h in host.values())

@@ -132,7 +132,8 @@ class ColumnShard:
 
     def __init__(self, spec: ColumnSpec, cell_lo: int, cell_hi: int, options_for=None,
                  concurrent_soma: bool = False, reset: bool = True, host: dict | None = None,
-                 runners: dict | None = None, grouped_soma: bool = False, schedule: str | None = None):
+                 runners: dict | None = None, grouped_soma: bool = False, schedule: str | None = None,
+                 layout: dict | None = None):
         from . import runtime as rt
         from .runner import CudaRunner, NodeArrays
 
@@ -143,7 +144,11 @@ class ColumnShard:
         self.spec = spec
         self.reset = reset
         self.cells = (cell_lo, cell_hi)
-        lay = shard_layout(spec, cell_lo, cell_hi)
+        # `layout`: shard_layout(spec, cell_lo, cell_hi) computed by the caller
+        # (the node_index / node_v inputs, like `host` for the stores)
+        lay = shard_layout(spec, cell_lo, cell_hi) if layout is None else layout
+        if lay["n_nodes"] != (cell_hi - cell_lo) * spec.nodes_per_cell:
+            raise ValueError("layout is for another shard")
         self.layout = lay
         irs = load_irs()
         self.runners, self.devs, self.node_index = {}, {}, {}
@@ -320,19 +325,20 @@ class ColumnShard:
 def simulate_column(spec: ColumnSpec, steps: int, cell_lo: int = 0, cell_hi: int | None = None,
                     host: dict | None = None, options_for=None, runners: dict | None = None,
                     reset: bool = True, concurrent_soma: bool = False, grouped_soma: bool = False,
-                    schedule: str | None = None):
+                    schedule: str | None = None, layout: dict | None = None):
     """Public column call (configs[4]): upload the stores of cells
     [cell_lo, cell_hi) (`host`, e.g. from host_stores(), ideally pinned),
     build the shared node layout on the device, nrn_init, `steps` timesteps
     of all populations, then download every store (in place, instance order)
     and the node arrays.  Returns (host, {"node_rhs", "node_d", "node_v"},
     shard).  Pass the previous call's `shard.runners` to reuse the loaded
-    kernels."""
+    kernels, and `layout` (shard_layout(spec, cell_lo, cell_hi): the node_index
+    and node_v inputs) to skip generating it."""
     cell_hi = spec.n_cells if cell_hi is None else cell_hi
     if host is None:
         host = host_stores(spec, cell_lo, cell_hi)
     shard = ColumnShard(spec, cell_lo, cell_hi, options_for, concurrent_soma=concurrent_soma, reset=reset,
-                        host=host, runners=runners, grouped_soma=grouped_soma, schedule=schedule)
+                        host=host, runners=runners, grouped_soma=grouped_soma, schedule=schedule, layout=layout)
     shard.launch(steps)
     shard.check()
     for stem in LAUNCH_ORDER:

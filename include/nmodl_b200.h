@@ -93,6 +93,13 @@ int nmodl_event_record_external(nmodl_event_t e, nmodl_stream_t s);
  * population order: rhs[node_index[j]] -= i_p[j], d[...] += g_p[j] */
 int nmodl_combine_unique(double *rhs, double *d, const int *node_index, long long n,
                          const double *const *i_ptrs, const double *const *g_ptrs, int n_pops, nmodl_stream_t s);
+/* the same fold; flags bit 0: launched for programmatic dependent launch
+ * behind the kernel before it on the stream -- the population currents are
+ * loaded at once, node rhs/d only after that kernel completes (it must not
+ * write any i_p/g_p array) */
+int nmodl_combine_unique_ex(double *rhs, double *d, const int *node_index, long long n,
+                            const double *const *i_ptrs, const double *const *g_ptrs, int n_pops, int flags,
+                            nmodl_stream_t s);
 int nmodl_event_sync(nmodl_event_t e);
 int nmodl_event_elapsed_ms(nmodl_event_t a, nmodl_event_t b, float *ms);
 /* CUDA-graph capture of the per-timestep launch loop */

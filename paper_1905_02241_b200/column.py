@@ -26,6 +26,8 @@ single-GPU column holds for those cells: shard checksums add up across ranks.
 
 from __future__ import annotations
 
+import os
+
 import zlib
 from dataclasses import dataclass
 from pathlib import Path
@@ -188,6 +190,10 @@ class ColumnShard:
         self.grouped = schedule == "grouped"
         self.concurrent = schedule != "sequential"
         self._soma_order = [m for m in LAUNCH_ORDER if m in SOMA_MECHS]
+        # the combine rides programmatic dependent launch when the kernels do
+        # and no memset sits between it and the kernel before it on the stream
+        self._combine_pdl = (all(r.options.pdl for r in self.runners.values()) and self._assign_first
+                             and os.environ.get("NMODL_COMBINE_PDL", "1") == "1")
         import ctypes as C
 
         if self.concurrent:
@@ -239,9 +245,13 @@ class ColumnShard:
 
         first = self.devs[self._soma_order[0]]
         nb = first.nodes
-        rt.check(L.nmodl_combine_unique(C.c_void_p(nb.node_rhs), C.c_void_p(nb.node_d), C.c_void_p(nb.node_index),
-                                        first.n, self._iptr, self._gptr, len(self._soma_order),
-                                        C.c_void_p(self.stream.handle)), "combine_unique")
+        # programmatic dependent launch behind the kernel before it on the main
+        # stream (Ih, or the previous step's synapses), which writes none of the
+        # soma currents: their loads overlap its tail, the fold waits for it
+        flags = 1 if self._combine_pdl else 0
+        rt.check(L.nmodl_combine_unique_ex(C.c_void_p(nb.node_rhs), C.c_void_p(nb.node_d), C.c_void_p(nb.node_index),
+                                           first.n, self._iptr, self._gptr, len(self._soma_order), flags,
+                                           C.c_void_p(self.stream.handle)), "combine_unique")
 
     def launch(self, steps: int = 1) -> None:
         import ctypes as C

@@ -629,38 +629,108 @@ struct nmodl_combine_args {
   const double* g[8];
   int n_pops;
 };
+// P populations known at compile time: every population's i/g load of a
+// node is in flight at once (a runtime-bounded loop issued them one L2
+// round trip after another: 5 populations took ~2 us at 12.5k nodes); the
+// arithmetic is the same chain in the same order.  PDL (flags bit 0): the
+// grid is launched for programmatic dependent launch behind the kernel
+// before it on the stream, loads the population currents (complete: they
+// come from full dependencies, e.g. another stream's kernel joined by an
+// event) and waits for that kernel only before it touches node rhs/d --
+// the caller vouches that the predecessor writes no i/g array it reads.
+template <int P, bool PDL>
 __global__ void k_combine_unique(double* __restrict__ rhs, double* __restrict__ d, const int* __restrict__ node_index,
                                  long long n, const nmodl_combine_args a) {
   // a following kernel launched for programmatic dependent launch (the
   // synapse step, CudaOptions.pdl) may be scheduled now; it waits for this
   // grid's completion before it reads anything
   asm volatile("griddepcontrol.launch_dependents;");
-  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (PDL) {
+    // one node per thread (the launch covers n): loads before the wait
+    double iv[P], gv[P];
+    int nd = 0;
+    if (j < n) {
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        iv[p] = __ldcg(a.i[p] + j);
+        gv[p] = __ldcg(a.g[p] + j);
+      }
+      nd = node_index[j];
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (j < n) {
+      double r = rhs[nd], dd = d[nd];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        r = r - iv[p];
+        dd = dd + gv[p];
+      }
+      rhs[nd] = r;
+      d[nd] = dd;
+    }
+    return;
+  }
+  for (; j < n; j += stride) {
+    double iv[P], gv[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      iv[p] = __ldcg(a.i[p] + j);
+      gv[p] = __ldcg(a.g[p] + j);
+    }
     const int nd = node_index[j];
     double r = rhs[nd], dd = d[nd];
-    for (int p = 0; p < a.n_pops; ++p) {
-      r = r - a.i[p][j];
-      dd = dd + a.g[p][j];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      r = r - iv[p];
+      dd = dd + gv[p];
     }
     rhs[nd] = r;
     d[nd] = dd;
   }
 }
-NMODL_API int nmodl_combine_unique(double* rhs, double* d, const int* node_index, long long n,
-                                   const double* const* i_ptrs, const double* const* g_ptrs, int n_pops,
-                                   cudaStream_t s) {
+NMODL_API int nmodl_combine_unique_ex(double* rhs, double* d, const int* node_index, long long n,
+                                      const double* const* i_ptrs, const double* const* g_ptrs, int n_pops, int flags,
+                                      cudaStream_t s) {
   if (n_pops < 0 || n_pops > 8) return (int)cudaErrorInvalidValue;
-  if (n <= 0) return 0;
+  if (n <= 0 || n_pops == 0) return 0;  // nothing to fold
   nmodl_combine_args a{};
   for (int p = 0; p < n_pops; ++p) {
     a.i[p] = i_ptrs[p];
     a.g[p] = g_ptrs[p];
   }
   a.n_pops = n_pops;
-  long long blocks = (n + 255) / 256;
-  k_combine_unique<<<(int)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, s>>>(rhs, d, node_index, n, a);
+  const long long blocks = (n + 255) / 256;
+  const bool pdl = (flags & 1) != 0;
+  if (pdl && blocks > (1LL << 30)) return (int)cudaErrorInvalidValue;
+  const int grid = pdl ? (int)blocks : (int)(blocks < 148 * 16 ? blocks : 148 * 16);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  switch (n_pops) {
+#define NM_COMBINE(P)                                                                                          \
+  case P:                                                                                                      \
+    if (pdl) CK(cudaLaunchKernelEx(&cfg, k_combine_unique<P, true>, rhs, d, node_index, n, a));                \
+    else CK(cudaLaunchKernelEx(&cfg, k_combine_unique<P, false>, rhs, d, node_index, n, a));                   \
+    break;
+    NM_COMBINE(1) NM_COMBINE(2) NM_COMBINE(3) NM_COMBINE(4) NM_COMBINE(5) NM_COMBINE(6) NM_COMBINE(7)
+    NM_COMBINE(8)
+#undef NM_COMBINE
+  }
   CK(cudaGetLastError());
   return 0;
+}
+NMODL_API int nmodl_combine_unique(double* rhs, double* d, const int* node_index, long long n,
+                                   const double* const* i_ptrs, const double* const* g_ptrs, int n_pops,
+                                   cudaStream_t s) {
+  return nmodl_combine_unique_ex(rhs, d, node_index, n, i_ptrs, g_ptrs, n_pops, 0, s);
 }
 
 

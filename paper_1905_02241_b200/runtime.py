@@ -72,6 +72,8 @@ _SIGS = {
     "nmodl_nccl_allgather_f64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]),
     "nmodl_combine_unique": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p,
                                        C.c_int, C.c_void_p]),
+    "nmodl_combine_unique_ex": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p,
+                                          C.c_int, C.c_int, C.c_void_p]),
     "nmodl_event_sync": (C.c_int, [C.c_void_p]),
     "nmodl_event_elapsed_ms": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_float)]),
     "nmodl_capture_begin": (C.c_int, [C.c_void_p]),

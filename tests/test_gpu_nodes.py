@@ -301,3 +301,45 @@ def test_simulate_skips_unused_arrays_the_same_way():
     with pytest.raises(InterpError) as got:
         simulate(ir, bad.copy(), 5, runner=r)
     assert str(got.value) == str(want.value)
+
+
+@pytest.mark.parametrize("flags", [0, 1])
+@pytest.mark.parametrize("n_pops", [1, 2, 5, 8])
+def test_combine_unique_in_population_order(n_pops, flags):
+    """nmodl_combine_unique_ex (plain and programmatic launch) folds the
+    populations' currents into node rhs/d in population order: bit-identical
+    to rhs -= i_0; rhs -= i_1; ... on the host; nodes without an instance
+    are left alone."""
+    import ctypes as C
+
+    from paper_1905_02241_b200 import runtime as rt
+
+    rng = np.random.default_rng(7 + n_pops)
+    n, n_nodes = 3001, 4000
+    node_index = rng.permutation(n_nodes)[:n].astype(np.int32)  # one instance per node
+    rhs0, d0 = rng.standard_normal(n_nodes), rng.standard_normal(n_nodes)
+    cur_i = [rng.standard_normal(n) * 10.0 ** rng.integers(-6, 6) for _ in range(n_pops)]
+    cur_g = [rng.random(n) * 10.0 ** rng.integers(-6, 6) for _ in range(n_pops)]
+    s = rt.Stream()
+
+    def up(a):
+        a = np.ascontiguousarray(a)
+        b = rt.DeviceBuffer(a.nbytes)
+        rt.h2d(b.ptr, a.ctypes.data, a.nbytes, s)
+        return b
+
+    bufs = [up(rhs0), up(d0), up(node_index)] + [up(a) for a in cur_i] + [up(a) for a in cur_g]
+    ip = (C.c_void_p * n_pops)(*[b.ptr for b in bufs[3:3 + n_pops]])
+    gp = (C.c_void_p * n_pops)(*[b.ptr for b in bufs[3 + n_pops:]])
+    L = rt.lib()
+    rt.check(L.nmodl_combine_unique_ex(C.c_void_p(bufs[0].ptr), C.c_void_p(bufs[1].ptr), C.c_void_p(bufs[2].ptr), n,
+                                       ip, gp, n_pops, flags, C.c_void_p(s.handle)), "combine_unique_ex")
+    rhs, d = np.empty(n_nodes), np.empty(n_nodes)
+    rt.d2h(rhs.ctypes.data, bufs[0].ptr, rhs.nbytes, s)
+    rt.d2h(d.ctypes.data, bufs[1].ptr, d.nbytes, s)
+    s.sync()
+    er, ed = rhs0.copy(), d0.copy()
+    for p in range(n_pops):
+        er[node_index] = er[node_index] - cur_i[p]
+        ed[node_index] = ed[node_index] + cur_g[p]
+    assert np.array_equal(rhs, er) and np.array_equal(d, ed)

@@ -6,7 +6,9 @@ RELAXED = [dict(recip=True), dict(div_approx=True), dict(recip=True, div_approx=
            dict(exp_smem=True, pipe=True, grid_waves=0),
            dict(recip=True, div_approx=True, pipe=True, fast_redo=True, ilp=2),
            dict(recip=True, quot=True, div_approx=True, exp_share=True, pipe=True, fast_redo=True),
-           dict(recip=True, quot=True, exp_share=True, exp_smem=True, fast_path=False)]
+           dict(recip=True, quot=True, exp_share=True, exp_smem=True, fast_path=False),
+           dict(lu_approx=True, lu_spec=True, pipe=True, fast_redo=True),
+           dict(lu_approx=True, div_approx=True)]
 RELAXED_STEMS = ["hh_subset", "NaTs2_t", "Ca_HVA", "Ih", "na6", "cdp5ish", "ProbAMPANMDA_EMS",
                  "corpus_cat", "corpus_vtrap", "corpus_kdr", "K_Pst", "SKv3_1"]
 PIPE_STEMS = ["hh_subset", "NaTs2_t", "na6", "cdp5ish", "ProbAMPANMDA_EMS", "corpus_cat", "cadyn"]

@@ -6,11 +6,14 @@ RELAXED = [dict(recip=True), dict(div_approx=True), dict(recip=True, div_approx=
            dict(exp_smem=True, pipe=True, grid_waves=0),
            dict(recip=True, div_approx=True, pipe=True, fast_redo=True, ilp=2),
            dict(recip=True, quot=True, div_approx=True, exp_share=True, pipe=True, fast_redo=True),
-           dict(recip=True, quot=True, exp_share=True, exp_smem=True, fast_path=False),
-           dict(lu_approx=True, lu_spec=True, pipe=True, fast_redo=True),
-           dict(lu_approx=True, div_approx=True)]
+           dict(recip=True, quot=True, exp_share=True, exp_smem=True, fast_path=False)]
 RELAXED_STEMS = ["hh_subset", "NaTs2_t", "Ca_HVA", "Ih", "na6", "cdp5ish", "ProbAMPANMDA_EMS",
                  "corpus_cat", "corpus_vtrap", "corpus_kdr", "K_Pst", "SKv3_1"]
+# relaxed solver-core quotients (CudaOptions.lu_approx) on the Newton / linear
+# solver fixtures; na6 is left out: its tiny occupancies take it to 1.1e-10
+# (profiles/r03/lu_approx.jsonl), so bench.py keeps IEEE pivots there
+LU_APPROX = [dict(lu_approx=True, lu_spec=True, pipe=True, fast_redo=True), dict(lu_approx=True, div_approx=True)]
+LU_APPROX_STEMS = ["cdp5ish", "corpus_cacum", "corpus_fourstate", "corpus_nonlin2", "corpus_nonlininit", "corpus_pump"]
 PIPE_STEMS = ["hh_subset", "NaTs2_t", "na6", "cdp5ish", "ProbAMPANMDA_EMS", "corpus_cat", "cadyn"]
 WAVES_STEMS = ["hh_subset", "NaTs2_t", "cdp5ish", "ProbAMPANMDA_EMS"]
 
@@ -69,5 +72,8 @@ def variants():
         out.append((st, kw))
     for st in RELAXED_STEMS:
         for r in RELAXED:
+            out.append((st, {"fast_path": True, **r}))
+    for st in LU_APPROX_STEMS:
+        for r in LU_APPROX:
             out.append((st, {"fast_path": True, **r}))
     return out

@@ -10,10 +10,14 @@ RELAXED = [dict(recip=True), dict(div_approx=True), dict(recip=True, div_approx=
 RELAXED_STEMS = ["hh_subset", "NaTs2_t", "Ca_HVA", "Ih", "na6", "cdp5ish", "ProbAMPANMDA_EMS",
                  "corpus_cat", "corpus_vtrap", "corpus_kdr", "K_Pst", "SKv3_1"]
 # relaxed solver-core quotients (CudaOptions.lu_approx) on the Newton / linear
-# solver fixtures; na6 is left out: its tiny occupancies take it to 1.1e-10
-# (profiles/r03/lu_approx.jsonl), so bench.py keeps IEEE pivots there
-LU_APPROX = [dict(lu_approx=True, lu_spec=True, pipe=True, fast_redo=True), dict(lu_approx=True, div_approx=True)]
+# solver fixtures.  na6 only with the LU multipliers relaxed (mode 2): its
+# back-substitution divides by tiny pivots and takes it to 1.1e-10 in modes
+# 1 / 3 (profiles/r03/lu_approx.jsonl), so bench.py uses mode 2 there
+LU_APPROX = [dict(lu_approx=1, lu_spec=True, pipe=True, fast_redo=True), dict(lu_approx=1, div_approx=True)]
 LU_APPROX_STEMS = ["cdp5ish", "corpus_cacum", "corpus_fourstate", "corpus_nonlin2", "corpus_nonlininit", "corpus_pump"]
+LU_APPROX_CASES = ([(st, v) for st in LU_APPROX_STEMS for v in LU_APPROX]
+                   + [(st, dict(lu_approx=2, lu_spec=True, pipe=True, fast_redo=True)) for st in ("na6", "corpus_fourstate")]
+                   + [("na6", dict(lu_approx=2))])
 PIPE_STEMS = ["hh_subset", "NaTs2_t", "na6", "cdp5ish", "ProbAMPANMDA_EMS", "corpus_cat", "cadyn"]
 WAVES_STEMS = ["hh_subset", "NaTs2_t", "cdp5ish", "ProbAMPANMDA_EMS"]
 
@@ -73,7 +77,6 @@ def variants():
     for st in RELAXED_STEMS:
         for r in RELAXED:
             out.append((st, {"fast_path": True, **r}))
-    for st in LU_APPROX_STEMS:
-        for r in LU_APPROX:
-            out.append((st, {"fast_path": True, **r}))
+    for st, r in LU_APPROX_CASES:
+        out.append((st, {"fast_path": True, **r}))
     return out

@@ -484,3 +484,23 @@ def test_direct_population_group_text():
     with pytest.raises(ValueError):
         emit_group("bad", [[(load_ir("Ca_HVA"), CudaOptions(ilp=2)), (load_ir("cadyn"), CudaOptions(ilp=1))]],
                    kind="direct")
+
+
+def test_lu_approx_modes_touch_only_the_solver_quotients():
+    """CudaOptions.lu_approx: 0 leaves the emitted text of every solver as
+    before (no NM_DIVM; build keys and ncu records stay valid); 2 routes only
+    the LU multipliers through NM_DIVM (relaxed in the fast pass, IEEE in the
+    exact redo) and keeps the back-substitution on NM_DIVX; 1 relaxes
+    NM_DIVX itself in the fast pass."""
+    from paper_1905_02241_b200.codegen_cuda import CudaOptions, emit_cuda
+
+    ir = load_ir("na6")
+    text = {m: emit_cuda(ir, CudaOptions(fast_path=True, lu_approx=m)).text for m in (0, 1, 2)}
+    assert "NM_DIVM" not in text[0] and "NM_DIVM" not in text[1]
+    mult = re.findall(r"const double f = (NM_DIV\w)\(", text[2])
+    assert mult and set(mult) == {"NM_DIVM"}
+    assert re.search(r"= NM_DIVX\(", text[2])  # back-substitution keeps the IEEE-capable macro
+    assert "#define NM_DIVM(a, b) (FAST ? nmodl::div_af" in text[2]
+    assert "#define NM_DIVX(a, b) (FAST ? nmodl::div_f(" in text[2]
+    assert "#define NM_DIVX(a, b) (FAST ? nmodl::div_af" in text[1]
+    assert text[0] == emit_cuda(ir, CudaOptions(fast_path=True)).text
